@@ -1,0 +1,31 @@
+# Build for the B200 FFTMatvec (sm_100a). `make` builds:
+#   paper_2508_10202_b200/libfftmv_cuda.so  -- the product (C ABI: include/fftmv_cuda.h)
+#   build/fftmv_cpp_tests                   -- C++ drop-in header tests (include/fftmv/*.hpp)
+#   oracle/liboracle.so, oracle/_ref/libfftmv_ref.so -- test-only checkers (oracle/Makefile)
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr -Xptxas -v
+PKG := paper_2508_10202_b200
+SRC := $(wildcard $(PKG)/csrc/*.cu) $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.cpp) include/fftmv_cuda.h
+
+all: lib oracle cpp
+
+lib: $(PKG)/libfftmv_cuda.so
+
+$(PKG)/libfftmv_cuda.so: $(SRC)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(PKG)/csrc/fmv_capi.cu $(PKG)/csrc/fmv_host.cpp -ldl -lcudart 2> build_ptxas.log || (cat build_ptxas.log; false)
+
+oracle:
+	$(MAKE) -C oracle all
+
+cpp: build/fftmv_cpp_tests
+
+build/fftmv_cpp_tests: tests/cpp/test_dropin.cpp $(wildcard include/fftmv/*.hpp) include/fftmv_cuda.h $(PKG)/libfftmv_cuda.so
+	@mkdir -p build
+	g++ -std=c++20 -O2 -Wall -Iinclude -o $@ tests/cpp/test_dropin.cpp -L$(PKG) -lfftmv_cuda -Wl,-rpath,'$$ORIGIN/../$(PKG)' -L/usr/local/cuda/lib64 -lcudart
+
+clean:
+	rm -f $(PKG)/libfftmv_cuda.so build/fftmv_cpp_tests
+	$(MAKE) -C oracle clean
+
+.PHONY: all lib oracle cpp clean

@@ -1,0 +1,134 @@
+/* fftmv_cuda.h -- C ABI of libfftmv_cuda.so, the B200 (sm_100a) FFTMatvec.
+ *
+ * This is the drop-in boundary for the reference's FFTMatvec path
+ * (/root/reference/proj/include/fftmv). Plain C types only: opaque handles,
+ * pointers, sizes, 5-char precision configs. The C++ header set in
+ * include/fftmv/ re-exposes the reference's C++ API (namespace fftmv) on top
+ * of these functions; INTEGRATION.md shows the bindings.
+ *
+ * Conventions (same as the reference):
+ *   - operator block column: col[t*nd*nm + i + j*nd]            (operator.hpp:28-29)
+ *   - spectral bins: bins[(k*nd*nm + i + j*nd)] complex, interleaved  (operator.hpp:58)
+ *   - vectors SOTI: m[c*nt + t], d[r*nt + t], always double at the I/O boundary
+ *                                                                (matvec.hpp:291-299)
+ *   - cfg: 5 chars, positions = phases {pad/broadcast, fft, sbgemv, ifft,
+ *     unpad/reduce} (config.hpp:14-33), chars 'd' or 's', plus the 'h' (fp16)
+ *     extension at positions 0, 2 and 4.
+ * Return codes: FMV_OK, or an error code with a message in fmv_last_error()
+ * (thread-local). The C++ wrapper maps FMV_EINVAL to std::invalid_argument
+ * and everything else to std::runtime_error, like the reference.
+ * Threading: an fmv_op is read-only after creation (materialization is
+ * internally synchronized) and may be shared by any number of contexts; an
+ * fmv_ctx (one CUDA stream + workspace) is used by one host thread at a time.
+ */
+#ifndef FFTMV_CUDA_H
+#define FFTMV_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMV_OK 0
+#define FMV_EINVAL 1
+#define FMV_ECUDA 2
+#define FMV_ENCCL 3
+#define FMV_ENOMEM 4
+#define FMV_EUNSUPPORTED 5
+
+#define FMV_FORWARD 0 /* d = F m   (matvec.hpp:305-310) */
+#define FMV_ADJOINT 1 /* m = F* d  (matvec.hpp:313-318) */
+
+#define FMV_GEMV_N 0 /* GemvMode::NoTrans   (gemv.hpp:33) */
+#define FMV_GEMV_T 1 /* GemvMode::Trans */
+#define FMV_GEMV_C 2 /* GemvMode::ConjTrans */
+
+typedef struct fmv_ctx fmv_ctx;
+typedef struct fmv_op fmv_op;
+
+/* PhaseTimings (matvec.hpp:42-51): seconds per phase + total. On B200 the
+ * phases are fused, so: [0] host->device copy of the input (0 when the I/O is
+ * device-resident), [1] pad+cast+r2c kernel, [2] SBGEMV kernel incl. both
+ * fused reorders, [3] c2r+unpad kernel, [4] device->host copy (+ reduce for
+ * the partitioned forward). */
+typedef struct {
+  double phase_s[5];
+  double total_s;
+} fmv_phase_times;
+
+const char* fmv_last_error(void);
+const char* fmv_version(void);
+
+/* ---- contexts: one device, one stream, a grow-only workspace ---- */
+/* stream: a cudaStream_t to run on, or NULL for a new non-blocking stream. */
+int fmv_ctx_create(int device, void* stream, fmv_ctx** out);
+int fmv_ctx_destroy(fmv_ctx* ctx);
+void* fmv_ctx_stream(fmv_ctx* ctx);
+/* Kernel-launch bookkeeping for benchmarks: total launches issued by this
+ * context, and (when profiling is on) per-kernel-class CUDA-event time. */
+uint64_t fmv_ctx_launches(fmv_ctx* ctx);
+int fmv_ctx_set_profiling(fmv_ctx* ctx, int enable);
+/* kernel classes: 0 r2c, 1 sbgemv-N, 2 sbgemv-C, 3 c2r, 4 other */
+int fmv_ctx_profile_read(fmv_ctx* ctx, double* ms_per_class5, uint64_t* launches_per_class5, int reset);
+int fmv_synchronize(fmv_ctx* ctx);
+
+/* ---- operator: setup_operator (operator.hpp:99-125) ---- */
+/* col: nt*nd*nm doubles (host, or device if col_on_device). */
+int fmv_op_create(fmv_ctx* ctx, size_t nm, size_t nd, size_t nt, const double* col, int col_on_device,
+                  fmv_op** out);
+int fmv_op_destroy(fmv_op* op);
+int fmv_op_dims(const fmv_op* op, size_t* nm, size_t* nd, size_t* nt);
+/* materialize_single (operator.hpp:90-93); prec 's' (fp32) or 'h' (fp16 ext.). Idempotent. */
+int fmv_op_materialize(fmv_ctx* ctx, fmv_op* op, char prec);
+int fmv_op_has(const fmv_op* op, char prec);
+/* Copy the bins to host in the reference layout: prec 'd' -> nb*nd*nm complex
+ * doubles (bins_double, operator.hpp:59); 's' -> complex floats. */
+int fmv_op_download_bins(fmv_ctx* ctx, const fmv_op* op, char prec, void* host_out);
+size_t fmv_op_device_bytes(const fmv_op* op);
+
+/* ---- matvecs: run_pipeline (matvec.hpp:233-289) ---- */
+/* Blocking, like the reference. in/out: double SOTI vectors; host pointers
+ * (pinned or pageable) unless io_on_device. times may be NULL. */
+int fmv_matvec(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* in, double* out,
+               int io_on_device, fmv_phase_times* times);
+/* Non-blocking variant: device pointers only, enqueued on the ctx stream. */
+int fmv_matvec_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* d_in, double* d_out);
+
+/* ---- casts (precision.hpp:27-39): logical conversion passes performed ---- */
+uint64_t fmv_casts_performed(void);
+void fmv_reset_cast_counter(void);
+
+/* ---- strided-batched GEMV (gemv.hpp:206-240), device pointers ----
+ * dtype 's','d','c','z' (or 'h' = complex fp16 storage, fp32 accumulation,
+ * output complex float). Strides/lda in elements. Returns the kernel used in
+ * *kernel_used (0 staged/TMA, 1 simple) when non-NULL. A and x must be
+ * readable up to the next 16-byte boundary past their last element. */
+int fmv_sbgemv(fmv_ctx* ctx, int mode, char dtype, size_t m, size_t n, size_t batch, size_t lda, size_t stride_a,
+               const void* A, size_t stride_x, const void* x, size_t stride_y, void* y, int force_simple,
+               int* kernel_used);
+
+/* ---- 1 x p partition over NCCL (partition.hpp:23-217) ---- */
+int fmv_comm_unique_id(void* out128);
+/* id128: the bytes from rank 0's fmv_comm_unique_id (exchange them out of band). */
+int fmv_comm_init(fmv_ctx* ctx, int nranks, int rank, const void* id128);
+int fmv_comm_destroy(fmv_ctx* ctx);
+/* Each rank holds the operator shard of its Grid1xP column range.
+ * FORWARD: in = this rank's m slice (shard_nm*nt), out = full d (nd*nt) on
+ *   every rank, partial d summed in cfg[4] precision (partition.hpp:157-182).
+ * ADJOINT: in = full d (nd*nt, read on rank 0 only), broadcast in cfg[0]
+ *   precision; out = this rank's m slice (partition.hpp:187-217). */
+int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* shard, int kind, const char* cfg, const double* in,
+                           double* out, int io_on_device, fmv_phase_times* times);
+
+/* ---- host helpers kept from the reference API ---- */
+uint64_t fmv_seed_stream(uint64_t seed, uint64_t stream);                          /* random_fill.hpp:30-32 */
+void fmv_uniform_fill(size_t count, uint64_t seed, double lo, double hi, double* out); /* random_fill.hpp:17-27 */
+int fmv_non_representable_fill(size_t count, uint64_t seed, double* out);           /* sweep.hpp:32-46 */
+int fmv_relative_error(size_t n, const double* x, const double* ref, double* out);  /* sweep.hpp:49-59 */
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,1110 @@
+// fmv_capi.cu -- host runtime behind include/fftmv_cuda.h.
+//
+// Owns device memory for spectral operators, per-context workspaces and
+// streams, launches the fused sm_100a kernels of the five-phase pipeline
+// (matvec.hpp:233-289) and the 1 x p NCCL partition (partition.hpp:141-217).
+// No CPU fallback exists: every compute entry point launches CUDA kernels
+// and fails loudly on any CUDA error.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/fftmv_cuda.h"
+#include "fmv_common.cuh"
+#include "fmv_fft.cuh"
+#include "fmv_sbgemv.cuh"
+
+using namespace fmv;
+
+// ======================================================================
+// errors
+// ======================================================================
+namespace {
+thread_local std::string g_err;
+
+struct FmvError {
+  int code;
+  std::string msg;
+};
+[[noreturn]] void fail(int code, const std::string& m) { throw FmvError{code, m}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    fail(e == cudaErrorMemoryAllocation ? FMV_ENOMEM : FMV_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+#define CK(x) ck((x), #x)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return FMV_OK;
+  } catch (const FmvError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return FMV_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FMV_ECUDA;
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    CK(cudaGetDevice(&prev));
+    if (prev != dev) CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+std::atomic<uint64_t> g_casts{0};
+
+int prec_of(char c) {
+  switch (c) {
+    case 'd': return PD;
+    case 's': return PS;
+    case 'h': return PH;
+    default: fail(FMV_EINVAL, std::string("precision config: invalid character '") + c + "'");
+  }
+}
+
+// config.hpp:36-51 plus the 'h' extension rules.
+std::array<int, 5> parse_cfg(const char* cfg) {
+  if (!cfg) fail(FMV_EINVAL, "precision config is null");
+  const size_t len = strnlen(cfg, 16);
+  if (len != 5)
+    fail(FMV_EINVAL, "precision config must be exactly 5 characters, got " + std::to_string(len));
+  std::array<int, 5> p{};
+  for (int i = 0; i < 5; ++i) {
+    if (cfg[i] != 'd' && cfg[i] != 's' && cfg[i] != 'h')
+      fail(FMV_EINVAL, std::string("precision config: invalid character '") + cfg[i] + "' at position " +
+                           std::to_string(i + 1) + " (expected 'd', 's' or 'h')");
+    p[i] = prec_of(cfg[i]);
+  }
+  if (p[1] == PH || p[3] == PH)
+    fail(FMV_EINVAL, "precision config: fp16 ('h') is supported for phases 1, 3 and 5 only (pad, sbgemv, unpad)");
+  return p;
+}
+
+// Logical cast passes of run_pipeline (matvec.hpp:88, :121-125, :163, :189-190).
+uint64_t count_casts(const std::array<int, 5>& p, bool payload) {
+  uint64_t n = 0;
+  if (!payload && p[0] != PD) ++n;
+  if (p[0] != p[1]) ++n;
+  if (p[1] != p[2]) ++n;
+  if (p[2] != p[3]) ++n;
+  if (p[3] != p[4]) ++n;
+  if (p[4] != PD) ++n;
+  return n;
+}
+
+size_t esize(int prec) { return prec == PD ? 16 : prec == PS ? 8 : 4; }
+
+// ======================================================================
+// FFT geometry + twiddle tables (per device, per L, per precision)
+// ======================================================================
+FftGeom make_geom(int Nt) {
+  FftGeom g{};
+  g.N = Nt;
+  g.L = 2 * Nt;
+  int n = Nt;
+  while (n > 1) {
+    int r;
+    if (n % 8 == 0 && n != 16) r = 8;  // 16 = 4*4 beats 8*2
+    else if (n % 4 == 0) r = 4;
+    else if (n % 2 == 0) r = 2;
+    else if (n % 5 == 0) r = 5;
+    else if (n % 3 == 0) r = 3;
+    else {
+      r = 7;
+      while (n % r) r += 2;  // smallest remaining odd prime factor >= 7
+    }
+    if (g.nst >= kMaxStages) fail(FMV_EUNSUPPORTED, "FFT: too many stages");
+    g.radix[g.nst++] = r;
+    n /= r;
+  }
+  return g;
+}
+
+struct TwiddleCache {
+  std::mutex mu;
+  std::map<std::tuple<int, int, int>, void*> tabs;  // (device, L, prec) -> device table
+  ~TwiddleCache() {}  // tables live for the process (like the reference's plan cache, fft.hpp:152-164)
+  const void* get(int dev, int L, int prec) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(dev, L, prec);
+    auto it = tabs.find(key);
+    if (it != tabs.end()) return it->second;
+    // exp(-2*pi*i*m/L), long double, exact at multiples of pi/2
+    std::vector<double> re(L), im(L);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int m = 0; m < L; ++m) {
+      long double c, s;
+      if ((4L * m) % L == 0) {
+        const int q = (int)((4L * m) / L);
+        const int cs[4] = {1, 0, -1, 0}, sn[4] = {0, -1, 0, 1};
+        c = cs[q];
+        s = sn[q];
+      } else {
+        const long double a = -2.0L * pi * (long double)m / (long double)L;
+        c = cosl(a);
+        s = sinl(a);
+      }
+      re[m] = (double)c;
+      im[m] = (double)s;
+      if (prec == PS) {
+        re[m] = (double)(float)c;
+        im[m] = (double)(float)s;
+      }
+    }
+    void* d = nullptr;
+    if (prec == PD) {
+      std::vector<double2> h(L);
+      for (int m = 0; m < L; ++m) h[m] = make_double2(re[m], im[m]);
+      CK(cudaMalloc(&d, L * sizeof(double2)));
+      CK(cudaMemcpy(d, h.data(), L * sizeof(double2), cudaMemcpyHostToDevice));
+    } else {
+      std::vector<float2> h(L);
+      for (int m = 0; m < L; ++m) h[m] = make_float2((float)re[m], (float)im[m]);
+      CK(cudaMalloc(&d, L * sizeof(float2)));
+      CK(cudaMemcpy(d, h.data(), L * sizeof(float2), cudaMemcpyHostToDevice));
+    }
+    tabs[key] = d;
+    return d;
+  }
+};
+TwiddleCache& twiddles() {
+  static TwiddleCache* c = new TwiddleCache;  // intentionally leaked: outlives static destructors
+  return *c;
+}
+
+// Raise a kernel's dynamic shared-memory cap once per (function, size).
+void prep_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> set;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = set[fn];
+  if (bytes > 48 * 1024 && bytes > cur) {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    cur = bytes;
+  }
+}
+
+int sm_count(int dev) {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  CK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  cache[dev] = n;
+  return n;
+}
+
+// ======================================================================
+// NCCL (dlopen'ed on first use: only the partitioned path needs it)
+// ======================================================================
+struct Nccl {
+  typedef int (*GetUniqueId)(void*);
+  typedef int (*CommInitRank)(void**, int, char[128], int);  // ncclUniqueId passed by value (128 bytes)
+  typedef int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+  typedef int (*Broadcast)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+  typedef int (*CommDestroy)(void*);
+  typedef const char* (*GetErrorString)(int);
+  void* h = nullptr;
+  GetUniqueId get_unique_id = nullptr;
+  void* comm_init_rank = nullptr;
+  AllReduce all_reduce = nullptr;
+  Broadcast broadcast = nullptr;
+  CommDestroy comm_destroy = nullptr;
+  GetErrorString err = nullptr;
+};
+Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names)
+      if ((n.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!n.h) return;
+    n.get_unique_id = (Nccl::GetUniqueId)dlsym(n.h, "ncclGetUniqueId");
+    n.comm_init_rank = dlsym(n.h, "ncclCommInitRank");
+    n.all_reduce = (Nccl::AllReduce)dlsym(n.h, "ncclAllReduce");
+    n.broadcast = (Nccl::Broadcast)dlsym(n.h, "ncclBroadcast");
+    n.comm_destroy = (Nccl::CommDestroy)dlsym(n.h, "ncclCommDestroy");
+    n.err = (Nccl::GetErrorString)dlsym(n.h, "ncclGetErrorString");
+  });
+  if (!n.h || !n.get_unique_id || !n.comm_init_rank || !n.all_reduce || !n.broadcast)
+    fail(FMV_ENCCL, "NCCL (libnccl.so.2) could not be loaded");
+  return n;
+}
+void nck(int rc, const char* what) {
+  if (rc != 0) fail(FMV_ENCCL, std::string(what) + ": " + (nccl().err ? nccl().err(rc) : "nccl error"));
+}
+// ncclDataType_t / ncclRedOp_t values (nccl.h)
+constexpr int kNcclHalf = 6, kNcclFloat = 7, kNcclDouble = 8, kNcclSum = 0;
+
+}  // namespace
+
+// ======================================================================
+// handles
+// ======================================================================
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    CK(cudaMalloc(&p, bytes));
+    n = bytes;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+};
+
+struct fmv_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  DevBuf x, y, io_in, io_out, partials, counters, payload, red;
+  size_t counters_len = 0;
+  uint64_t launches = 0;
+  bool profiling = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_pool;
+  double prof_ms[5] = {0, 0, 0, 0, 0};
+  uint64_t prof_n[5] = {0, 0, 0, 0, 0};
+  void* comm = nullptr;
+  int nranks = 1, rank = 0;
+  cudaEvent_t te[8] = {};
+
+  cudaEvent_t ev() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+  // Zeroed ticket counters for the SBGEMV-N cross-CTA reduction.
+  unsigned* tickets(size_t nbatch) {
+    if (nbatch > counters_len) {
+      counters.ensure(nbatch * sizeof(unsigned));
+      CK(cudaMemsetAsync(counters.p, 0, nbatch * sizeof(unsigned), stream));
+      counters_len = nbatch;
+    }
+    return static_cast<unsigned*>(counters.p);
+  }
+};
+
+struct fmv_op {
+  int device = 0;
+  size_t nm = 0, nd = 0, nt = 0;
+  void* bins_d = nullptr;  // double2, lda = nd
+  void* bins_s = nullptr;  // float2, lda = lda_s
+  void* bins_h = nullptr;  // __half2, lda = lda_h
+  size_t lda_s = 0, lda_h = 0;
+  std::mutex mu;
+  size_t nb() const { return nt + 1; }
+};
+
+namespace {
+
+// ---------------------------------------------------------------- launch --
+template <class Fn>
+void launch(fmv_ctx* ctx, int cls, Fn&& fn) {
+  ProfRec r{cls, nullptr, nullptr};
+  if (ctx->profiling) {
+    r.a = ctx->ev();
+    r.b = ctx->ev();
+    CK(cudaEventRecord(r.a, ctx->stream));
+  }
+  fn();
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  if (ctx->profiling) {
+    CK(cudaEventRecord(r.b, ctx->stream));
+    ctx->prof.push_back(r);
+  }
+}
+
+int fft_series_per_cta(int N, size_t celem) {
+  const size_t per = 2 * (size_t)(N + 1) * celem;
+  if (per > 200 * 1024)
+    fail(FMV_EUNSUPPORTED, "FFT: n_t = " + std::to_string(N) + " exceeds the shared-memory FFT capacity");
+  const size_t budget = 64 * 1024;
+  return (int)std::max<size_t>(1, std::min<size_t>(16, budget / per));
+}
+
+template <int C0, int C1, int C2, class Tin>
+void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, int Nt, void* out, long out_ks,
+           long out_ss) {
+  using R = typename PT<C1>::real;
+  using C = typename CT<R>::c;
+  const FftGeom g = make_geom(Nt);
+  const int S = fft_series_per_cta(g.N, sizeof(C));
+  const size_t smem = 2 * (size_t)S * (g.N + 1) * sizeof(C);
+  auto kern = k_r2c<C0, C1, C2, Tin>;
+  prep_smem((const void*)kern, smem);
+  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, g.L, C1));
+  const long grid = (nseries + S - 1) / S;
+  launch(ctx, 0, [&] {
+    kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(in, in_ss, in_ts, nseries, Nt,
+                                                     static_cast<typename PT<C2>::cplx*>(out), out_ks, out_ss, g, tw, S);
+  });
+}
+
+template <class Tin>
+void r2c_dispatch(fmv_ctx* ctx, int c0, int c1, int c2, const Tin* in, long in_ss, long in_ts, long nseries, int Nt,
+                  void* out, long out_ks, long out_ss) {
+#define R2C_CASE(A, B, C)                                                                 \
+  if (c0 == A && c1 == B && c2 == C) {                                                    \
+    r2c_t<A, B, C, Tin>(ctx, in, in_ss, in_ts, nseries, Nt, out, out_ks, out_ss);         \
+    return;                                                                               \
+  }
+  R2C_CASE(PD, PD, PD) R2C_CASE(PD, PD, PS) R2C_CASE(PD, PD, PH)
+  R2C_CASE(PD, PS, PD) R2C_CASE(PD, PS, PS) R2C_CASE(PD, PS, PH)
+  R2C_CASE(PS, PD, PD) R2C_CASE(PS, PD, PS) R2C_CASE(PS, PD, PH)
+  R2C_CASE(PS, PS, PD) R2C_CASE(PS, PS, PS) R2C_CASE(PS, PS, PH)
+  R2C_CASE(PH, PD, PD) R2C_CASE(PH, PD, PS) R2C_CASE(PH, PD, PH)
+  R2C_CASE(PH, PS, PD) R2C_CASE(PH, PS, PS) R2C_CASE(PH, PS, PH)
+#undef R2C_CASE
+  fail(FMV_EINVAL, "r2c: unsupported precision combination");
+}
+
+template <int C3, int C4>
+void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, int Nt, double* out, long out_ss) {
+  using C = typename PT<C3>::cplx;
+  const FftGeom g = make_geom(Nt);
+  const int S = fft_series_per_cta(g.N, sizeof(C));
+  const size_t smem = 2 * (size_t)S * (g.N + 1) * sizeof(C);
+  auto kern = k_c2r<C3, C4>;
+  prep_smem((const void*)kern, smem);
+  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, g.L, C3));
+  const long grid = (nseries + S - 1) / S;
+  launch(ctx, 3, [&] {
+    kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(static_cast<const C*>(in), in_ks, in_ss, nseries, Nt, out,
+                                                     out_ss, g, tw, S);
+  });
+}
+
+void c2r_dispatch(fmv_ctx* ctx, int c3, int c4, const void* in, long in_ks, long in_ss, long nseries, int Nt,
+                  double* out, long out_ss) {
+#define C2R_CASE(A, B)                                                  \
+  if (c3 == A && c4 == B) {                                             \
+    c2r_t<A, B>(ctx, in, in_ks, in_ss, nseries, Nt, out, out_ss);       \
+    return;                                                             \
+  }
+  C2R_CASE(PD, PD) C2R_CASE(PD, PS) C2R_CASE(PD, PH) C2R_CASE(PS, PD) C2R_CASE(PS, PS) C2R_CASE(PS, PH)
+#undef C2R_CASE
+  fail(FMV_EINVAL, "c2r: unsupported precision combination");
+}
+
+// ------------------------------------------------------------- SBGEMV ----
+struct GemvPlan {
+  GemvParams p{};
+  int block = 0;
+  size_t smem = 0;
+  int rpt = 1;
+};
+
+// Tunables (env overridable for on-GPU sweeps): A-stage bytes and ring depth.
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+template <int MODE, class E, class O, int RPT>
+void sbgemv_launch_t(fmv_ctx* ctx, GemvPlan& gp) {
+  auto kern = k_sbgemv<MODE, E, O, RPT>;
+  prep_smem((const void*)kern, gp.smem);
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, size_t>, int> occ_cache;
+  int occ = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(ctx->device, gp.block, gp.smem);
+    auto it = occ_cache.find(key);
+    if (it == occ_cache.end()) {
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, gp.block, gp.smem));
+      occ_cache[key] = occ;
+    } else {
+      occ = it->second;
+    }
+  }
+  if (occ < 1) fail(FMV_EUNSUPPORTED, "sbgemv: staged kernel does not fit on an SM");
+  const int ctas_per_sm = std::min(occ, env_int("FMV_SBGEMV_CTAS_PER_SM", 2));
+  long P = (long)sm_count(ctx->device) * ctas_per_sm;
+  P = std::min(P, gp.p.T);
+  gp.p.P = (int)P;
+  if (MODE == GM_N) {
+    const size_t part_bytes = (size_t)(P + gp.p.batch) * gp.p.m * sizeof(typename ET<E>::A);
+    ctx->partials.ensure(part_bytes);
+    gp.p.partials = ctx->partials.p;
+    gp.p.counters = ctx->tickets((size_t)gp.p.batch);
+  }
+  launch(ctx, MODE == GM_N ? 1 : 2, [&] { kern<<<(unsigned)P, gp.block, gp.smem, ctx->stream>>>(gp.p); });
+}
+
+template <int MODE, class E, class O>
+void sbgemv_simple_t(fmv_ctx* ctx, GemvPlan& gp) {
+  const long outs = MODE == GM_N ? gp.p.m : gp.p.n;
+  dim3 grid((unsigned)((outs + 127) / 128), (unsigned)gp.p.batch);
+  launch(ctx, MODE == GM_N ? 1 : 2, [&] { k_sbgemv_simple<MODE, E, O><<<grid, 128, 0, ctx->stream>>>(gp.p); });
+}
+
+constexpr int kConsumers = 256;  // consumer threads per CTA (+1 producer warp); __launch_bounds__(288, 2)
+
+// Fills the staged-kernel plan; returns false when the staged kernel's
+// limits (m <= 1024 rows for NoTrans, stage fits) are exceeded.
+bool plan_staged(GemvPlan& gp, int mode, size_t es, size_t accsz) {
+  GemvParams& p = gp.p;
+  const long col_bytes = p.lda * (long)es;
+  const int a_target = env_int("FMV_SBGEMV_STAGE_BYTES", 24 * 1024);
+  int Jc = (int)std::max<long>(1, a_target / std::max<long>(col_bytes, 1));
+  const long max_a = ((long)(Jc - 1) * p.lda + p.m) * (long)es;
+  if (max_a > 96 * 1024) return false;
+  p.Jc = Jc;
+  auto up128 = [](long v) { return (int)((v + 127) / 128 * 128); };
+  p.a_slot = up128(max_a + 32);
+  const long max_x = (mode == GM_N ? (long)Jc : (long)p.m) * (long)es;
+  p.x_slot = up128(max_x + 32);
+  p.nstage = std::max(2, std::min(16, env_int("FMV_SBGEMV_STAGES", 4)));
+  size_t red = 0;
+  if (mode == GM_N) {
+    int rpt = 1;
+    while ((p.m + rpt - 1) / rpt > kConsumers) rpt *= 2;
+    if (rpt > 4) return false;
+    p.RT = (p.m + rpt - 1) / rpt;
+    p.G = std::max(1, kConsumers / p.RT);
+    const int ncons = (p.RT * p.G + 31) / 32 * 32;
+    gp.block = ncons + 32;
+    gp.rpt = rpt;
+    red = (size_t)p.G * p.m * accsz;
+  } else {
+    p.LPC = p.m > 16 ? 32 : p.m > 8 ? 16 : p.m > 4 ? 8 : 4;
+    gp.block = kConsumers + 32;
+  }
+  gp.smem = 512 + (size_t)p.nstage * (p.a_slot + p.x_slot) + (red + 127) / 128 * 128;
+  if (gp.smem > 220 * 1024) return false;
+  return true;
+}
+
+template <int MODE, class E, class O>
+void sbgemv_run_t(fmv_ctx* ctx, GemvPlan& gp, bool force_simple, int* used) {
+  const bool staged = !force_simple && plan_staged(gp, MODE, sizeof(E), sizeof(typename ET<E>::A));
+  if (used) *used = staged ? 0 : 1;
+  if (!staged) {
+    sbgemv_simple_t<MODE, E, O>(ctx, gp);
+    return;
+  }
+  if constexpr (MODE == GM_N) {
+    if (gp.rpt == 1) sbgemv_launch_t<MODE, E, O, 1>(ctx, gp);
+    else if (gp.rpt == 2) sbgemv_launch_t<MODE, E, O, 2>(ctx, gp);
+    else sbgemv_launch_t<MODE, E, O, 4>(ctx, gp);
+  } else {
+    sbgemv_launch_t<MODE, E, O, 1>(ctx, gp);
+  }
+}
+
+template <class E, class O>
+void sbgemv_mode(fmv_ctx* ctx, int mode, GemvPlan& gp, bool force_simple, int* used) {
+  if (mode == GM_N) sbgemv_run_t<GM_N, E, O>(ctx, gp, force_simple, used);
+  else if (mode == GM_T) sbgemv_run_t<GM_T, E, O>(ctx, gp, force_simple, used);
+  else sbgemv_run_t<GM_C, E, O>(ctx, gp, force_simple, used);
+}
+
+GemvPlan make_gemv(const void* A, long m, long n, long batch, long lda, long sa, const void* x, long sx, void* y,
+                   long sy) {
+  GemvPlan gp;
+  GemvParams& p = gp.p;
+  p.A = static_cast<const unsigned char*>(A);
+  p.lda = lda;
+  p.sa = sa;
+  p.x = static_cast<const unsigned char*>(x);
+  p.sx = sx;
+  p.y = static_cast<unsigned char*>(y);
+  p.sy = sy;
+  p.m = (int)m;
+  p.n = n;
+  p.batch = batch;
+  p.T = batch * n;
+  return gp;
+}
+
+// ------------------------------------------------------------ pipeline ----
+const void* op_bins(fmv_ctx* ctx, fmv_op* op, int prec, long* lda);
+
+// run_pipeline (matvec.hpp:233-289) on device buffers, enqueued on ctx->stream.
+// payload_prec >= 0: `in` holds the broadcast payload already in that
+// precision (partition.hpp:198-212); otherwise `in` is double.
+void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5>& p, const void* in,
+              int payload_prec, double* out, cudaEvent_t ev_r2c = nullptr, cudaEvent_t ev_gemv = nullptr) {
+  fmv_op* op = const_cast<fmv_op*>(cop);
+  const bool fwd = kind == FMV_FORWARD;
+  const long nt = (long)op->nt, nb = (long)op->nb();
+  const long n_in = fwd ? (long)op->nm : (long)op->nd;
+  const long n_out = fwd ? (long)op->nd : (long)op->nm;
+  long lda = 0;
+  const void* bins = op_bins(ctx, op, p[2], &lda);
+  const size_t e2 = esize(p[2]), e3 = esize(p[3]);
+  ctx->x.ensure((size_t)nb * n_in * e2 + 256);
+  ctx->y.ensure((size_t)nb * n_out * e3 + 256);
+  // Phases 1-2 (+ reorder to TOSI, cast to cfg[2]).
+  if (payload_prec < 0)
+    r2c_dispatch<double>(ctx, p[0], p[1], p[2], static_cast<const double*>(in), nt, 1, n_in, (int)nt, ctx->x.p, n_in, 1);
+  else if (payload_prec == PD)
+    r2c_dispatch<double>(ctx, PD, p[1], p[2], static_cast<const double*>(in), nt, 1, n_in, (int)nt, ctx->x.p, n_in, 1);
+  else if (payload_prec == PS)
+    r2c_dispatch<float>(ctx, PS, p[1], p[2], static_cast<const float*>(in), nt, 1, n_in, (int)nt, ctx->x.p, n_in, 1);
+  else
+    r2c_dispatch<__half>(ctx, PH, p[1], p[2], static_cast<const __half*>(in), nt, 1, n_in, (int)nt, ctx->x.p, n_in, 1);
+  if (ev_r2c) CK(cudaEventRecord(ev_r2c, ctx->stream));
+  // Phase 3 SBGEMV in cfg[2], output cast to cfg[3], TOSI.
+  const long m = (long)op->nd, n = (long)op->nm;
+  GemvPlan gp = fwd ? make_gemv(bins, m, n, nb, lda, n * lda, ctx->x.p, n, ctx->y.p, m)
+                    : make_gemv(bins, m, n, nb, lda, n * lda, ctx->x.p, m, ctx->y.p, n);
+  const int mode = fwd ? GM_N : GM_C;
+  if (p[2] == PD) {
+    if (p[3] == PD) sbgemv_mode<double2, double2>(ctx, mode, gp, false, nullptr);
+    else sbgemv_mode<double2, float2>(ctx, mode, gp, false, nullptr);
+  } else if (p[2] == PS) {
+    if (p[3] == PD) sbgemv_mode<float2, double2>(ctx, mode, gp, false, nullptr);
+    else sbgemv_mode<float2, float2>(ctx, mode, gp, false, nullptr);
+  } else {
+    if (p[3] == PD) sbgemv_mode<__half2, double2>(ctx, mode, gp, false, nullptr);
+    else sbgemv_mode<__half2, float2>(ctx, mode, gp, false, nullptr);
+  }
+  if (ev_gemv) CK(cudaEventRecord(ev_gemv, ctx->stream));
+  // Phases 4-5 (+ reorder back to SOTI, 1/L in cfg[3], unpad, cast cfg[4]).
+  c2r_dispatch(ctx, p[3], p[4], ctx->y.p, n_out, 1, n_out, (int)nt, out, nt);
+  g_casts.fetch_add(count_casts(p, payload_prec >= 0), std::memory_order_relaxed);
+}
+
+// --------------------------------------------------------- cast kernels --
+template <class O>
+__global__ void k_cast_bins(const double2* __restrict__ in, O* __restrict__ out, long ncols, long nd, long lda_out) {
+  const long total = ncols * lda_out;
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const long c = e / lda_out, i = e - c * lda_out;
+    out[e] = i < nd ? cfrom_d<O>(in[c * nd + i]) : cfrom_d<O>(make_double2(0.0, 0.0));
+  }
+}
+template <class O>
+__global__ void k_unpad_bins(const O* __restrict__ in, long lda_in, O* __restrict__ out, long ncols, long nd) {
+  const long total = ncols * nd;
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const long c = e / nd, i = e - c * nd;
+    out[e] = in[c * lda_in + i];
+  }
+}
+__global__ void k_d2f(const double* __restrict__ in, float* __restrict__ out, long n) {
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x)
+    out[e] = __double2float_rn(in[e]);
+}
+__global__ void k_f2d(const float* __restrict__ in, double* __restrict__ out, long n) {
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x)
+    out[e] = (double)in[e];
+}
+__global__ void k_d2h(const double* __restrict__ in, __half* __restrict__ out, long n) {
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x)
+    out[e] = __double2half(in[e]);
+}
+
+unsigned grid_for(long n, int block, int dev) {
+  const long want = (n + block - 1) / block;
+  const long cap = (long)sm_count(dev) * 16;
+  return (unsigned)std::max<long>(1, std::min(want, cap));
+}
+
+void materialize(fmv_ctx* ctx, fmv_op* op, int prec) {
+  std::lock_guard<std::mutex> lk(op->mu);
+  if (prec == PS && op->bins_s) return;
+  if (prec == PH && op->bins_h) return;
+  const long ncols = (long)(op->nb() * op->nm);
+  const long nd = (long)op->nd;
+  // pad the leading dimension so every column starts 16-byte aligned (TMA)
+  const long lda = prec == PS ? (nd + 1) / 2 * 2 : (nd + 3) / 4 * 4;
+  const size_t bytes = (size_t)ncols * lda * (prec == PS ? 8 : 4) + 256;
+  void* p = nullptr;
+  CK(cudaMalloc(&p, bytes));
+  if (prec == PS) {
+    launch(ctx, 4, [&] {
+      k_cast_bins<float2><<<grid_for(ncols * lda, 256, ctx->device), 256, 0, ctx->stream>>>(
+          static_cast<const double2*>(op->bins_d), static_cast<float2*>(p), ncols, nd, lda);
+    });
+    op->bins_s = p;
+    op->lda_s = (size_t)lda;
+  } else {
+    launch(ctx, 4, [&] {
+      k_cast_bins<__half2><<<grid_for(ncols * lda, 256, ctx->device), 256, 0, ctx->stream>>>(
+          static_cast<const double2*>(op->bins_d), static_cast<__half2*>(p), ncols, nd, lda);
+    });
+    op->bins_h = p;
+    op->lda_h = (size_t)lda;
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  g_casts.fetch_add(1, std::memory_order_relaxed);  // ensure_single's cast_buffer (operator.hpp:72)
+}
+
+const void* op_bins(fmv_ctx* ctx, fmv_op* op, int prec, long* lda) {
+  if (prec == PD) {
+    *lda = (long)op->nd;
+    return op->bins_d;
+  }
+  if (prec == PS) {
+    if (!op->bins_s) materialize(ctx, op, PS);
+    *lda = (long)op->lda_s;
+    return op->bins_s;
+  }
+  if (!op->bins_h) materialize(ctx, op, PH);
+  *lda = (long)op->lda_h;
+  return op->bins_h;
+}
+
+}  // namespace
+
+// ======================================================================
+// C ABI
+// ======================================================================
+extern "C" {
+
+const char* fmv_last_error(void) { return g_err.c_str(); }
+const char* fmv_version(void) { return "fftmv-b200 0.1 (sm_100a)"; }
+
+int fmv_ctx_create(int device, void* stream, fmv_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(FMV_EINVAL, "fmv_ctx_create: out is null");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) fail(FMV_EINVAL, "fmv_ctx_create: bad device " + std::to_string(device));
+    DeviceGuard dg(device);
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      fail(FMV_EUNSUPPORTED, std::string("libfftmv_cuda is built for sm_100a (B200); device is ") + prop.name);
+    auto* c = new fmv_ctx;
+    c->device = device;
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    for (auto& e : c->te) CK(cudaEventCreate(&e));
+    *out = c;
+  });
+}
+
+int fmv_ctx_destroy(fmv_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    DeviceGuard dg(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto* b : {&ctx->x, &ctx->y, &ctx->io_in, &ctx->io_out, &ctx->partials, &ctx->counters, &ctx->payload,
+                    &ctx->red})
+      b->release();
+    for (auto& r : ctx->prof) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    for (auto e : ctx->te) cudaEventDestroy(e);
+    if (ctx->comm && nccl().comm_destroy) nccl().comm_destroy(ctx->comm);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+void* fmv_ctx_stream(fmv_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+uint64_t fmv_ctx_launches(fmv_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int fmv_ctx_set_profiling(fmv_ctx* ctx, int enable) {
+  return guarded([&] {
+    if (!ctx) fail(FMV_EINVAL, "null ctx");
+    ctx->profiling = enable != 0;
+  });
+}
+
+int fmv_ctx_profile_read(fmv_ctx* ctx, double* ms5, uint64_t* n5, int reset) {
+  return guarded([&] {
+    if (!ctx) fail(FMV_EINVAL, "null ctx");
+    DeviceGuard dg(ctx->device);
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (auto& r : ctx->prof) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, r.a, r.b));
+      ctx->prof_ms[r.cls] += ms;
+      ctx->prof_n[r.cls] += 1;
+      ctx->ev_pool.push_back(r.a);
+      ctx->ev_pool.push_back(r.b);
+    }
+    ctx->prof.clear();
+    for (int i = 0; i < 5; ++i) {
+      if (ms5) ms5[i] = ctx->prof_ms[i];
+      if (n5) n5[i] = ctx->prof_n[i];
+      if (reset) {
+        ctx->prof_ms[i] = 0;
+        ctx->prof_n[i] = 0;
+      }
+    }
+  });
+}
+
+int fmv_synchronize(fmv_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) fail(FMV_EINVAL, "null ctx");
+    DeviceGuard dg(ctx->device);
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int fmv_op_create(fmv_ctx* ctx, size_t nm, size_t nd, size_t nt, const double* col, int col_on_device, fmv_op** out) {
+  return guarded([&] {
+    if (!ctx || !out) fail(FMV_EINVAL, "fmv_op_create: null argument");
+    if (nm < 1 || nd < 1 || nt < 1) fail(FMV_EINVAL, "ProblemDims: all extents must be >= 1");
+    if (!col) fail(FMV_EINVAL, "fmv_op_create: null block column");
+    DeviceGuard dg(ctx->device);
+    std::unique_ptr<fmv_op> op(new fmv_op);
+    op->device = ctx->device;
+    op->nm = nm;
+    op->nd = nd;
+    op->nt = nt;
+    const size_t S = nd * nm, nb = nt + 1;
+    CK(cudaMalloc(&op->bins_d, nb * S * sizeof(double2) + 256));
+    const double* dcol = col;
+    void* tmp = nullptr;
+    if (!col_on_device) {
+      CK(cudaMalloc(&tmp, nt * S * sizeof(double)));
+      CK(cudaMemcpyAsync(tmp, col, nt * S * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      dcol = static_cast<const double*>(tmp);
+    }
+    // operator.hpp:99-125: every (i,j) series, time-outer in the column,
+    // padded to 2nt and r2c'd in fp64, written bin-major.
+    r2c_dispatch<double>(ctx, PD, PD, PD, dcol, 1, (long)S, (long)S, (int)nt, op->bins_d, (long)S, 1);
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (tmp) cudaFree(tmp);
+    *out = op.release();
+  });
+}
+
+int fmv_op_destroy(fmv_op* op) {
+  return guarded([&] {
+    if (!op) return;
+    DeviceGuard dg(op->device);
+    if (op->bins_d) cudaFree(op->bins_d);
+    if (op->bins_s) cudaFree(op->bins_s);
+    if (op->bins_h) cudaFree(op->bins_h);
+    delete op;
+  });
+}
+
+int fmv_op_dims(const fmv_op* op, size_t* nm, size_t* nd, size_t* nt) {
+  return guarded([&] {
+    if (!op) fail(FMV_EINVAL, "null op");
+    if (nm) *nm = op->nm;
+    if (nd) *nd = op->nd;
+    if (nt) *nt = op->nt;
+  });
+}
+
+int fmv_op_materialize(fmv_ctx* ctx, fmv_op* op, char prec) {
+  return guarded([&] {
+    if (!ctx || !op) fail(FMV_EINVAL, "null argument");
+    if (prec != 's' && prec != 'h') fail(FMV_EINVAL, "fmv_op_materialize: prec must be 's' or 'h'");
+    DeviceGuard dg(ctx->device);
+    materialize(ctx, op, prec_of(prec));
+  });
+}
+
+int fmv_op_has(const fmv_op* op, char prec) {
+  if (!op) return 0;
+  if (prec == 'd') return op->bins_d != nullptr;
+  if (prec == 's') return op->bins_s != nullptr;
+  if (prec == 'h') return op->bins_h != nullptr;
+  return 0;
+}
+
+int fmv_op_download_bins(fmv_ctx* ctx, const fmv_op* cop, char prec, void* host_out) {
+  return guarded([&] {
+    if (!ctx || !cop || !host_out) fail(FMV_EINVAL, "null argument");
+    fmv_op* op = const_cast<fmv_op*>(cop);
+    DeviceGuard dg(ctx->device);
+    const size_t ncols = op->nb() * op->nm;
+    if (prec == 'd') {
+      CK(cudaMemcpy(host_out, op->bins_d, ncols * op->nd * sizeof(double2), cudaMemcpyDeviceToHost));
+    } else if (prec == 's') {
+      if (!op->bins_s) materialize(ctx, op, PS);
+      CK(cudaMemcpy2D(host_out, op->nd * sizeof(float2), op->bins_s, op->lda_s * sizeof(float2),
+                      op->nd * sizeof(float2), ncols, cudaMemcpyDeviceToHost));
+    } else {
+      fail(FMV_EINVAL, "fmv_op_download_bins: prec must be 'd' or 's'");
+    }
+  });
+}
+
+size_t fmv_op_device_bytes(const fmv_op* op) {
+  if (!op) return 0;
+  const size_t ncols = op->nb() * op->nm;
+  size_t b = ncols * op->nd * sizeof(double2);
+  if (op->bins_s) b += ncols * op->lda_s * sizeof(float2);
+  if (op->bins_h) b += ncols * op->lda_h * sizeof(__half2);
+  return b;
+}
+
+int fmv_matvec_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* d_in, double* d_out) {
+  return guarded([&] {
+    if (!ctx || !op || !d_in || !d_out) fail(FMV_EINVAL, "fmv_matvec_async: null argument");
+    if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
+    const auto p = parse_cfg(cfg);
+    DeviceGuard dg(ctx->device);
+    pipeline(ctx, op, kind, p, d_in, -1, d_out);
+  });
+}
+
+int fmv_matvec(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* in, double* out,
+               int io_on_device, fmv_phase_times* times) {
+  return guarded([&] {
+    if (!ctx || !op || !in || !out) fail(FMV_EINVAL, "fmv_matvec: null argument");
+    if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
+    const auto p = parse_cfg(cfg);
+    DeviceGuard dg(ctx->device);
+    const bool fwd = kind == FMV_FORWARD;
+    const size_t n_in = (fwd ? op->nm : op->nd) * op->nt, n_out = (fwd ? op->nd : op->nm) * op->nt;
+    const double* din = in;
+    double* dout = out;
+    cudaStream_t s = ctx->stream;
+    auto* te = ctx->te;
+    if (times) CK(cudaEventRecord(te[0], s));
+    if (!io_on_device) {
+      ctx->io_in.ensure(n_in * sizeof(double));
+      ctx->io_out.ensure(n_out * sizeof(double));
+      CK(cudaMemcpyAsync(ctx->io_in.p, in, n_in * sizeof(double), cudaMemcpyHostToDevice, s));
+      din = static_cast<const double*>(ctx->io_in.p);
+      dout = static_cast<double*>(ctx->io_out.p);
+    }
+    if (times) CK(cudaEventRecord(te[1], s));
+    pipeline(ctx, op, kind, p, din, -1, dout, times ? te[2] : nullptr, times ? te[3] : nullptr);
+    if (times) CK(cudaEventRecord(te[4], s));
+    if (!io_on_device) CK(cudaMemcpyAsync(out, dout, n_out * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (times) CK(cudaEventRecord(te[5], s));
+    CK(cudaStreamSynchronize(s));
+    if (times) {
+      float ms[5];
+      CK(cudaEventElapsedTime(&ms[0], te[0], te[1]));
+      CK(cudaEventElapsedTime(&ms[1], te[1], te[2]));
+      CK(cudaEventElapsedTime(&ms[2], te[2], te[3]));
+      CK(cudaEventElapsedTime(&ms[3], te[3], te[4]));
+      CK(cudaEventElapsedTime(&ms[4], te[4], te[5]));
+      double tot = 0;
+      for (int i = 0; i < 5; ++i) {
+        times->phase_s[i] = ms[i] * 1e-3;
+        tot += times->phase_s[i];
+      }
+      times->total_s = tot;
+    }
+  });
+}
+
+uint64_t fmv_casts_performed(void) { return g_casts.load(std::memory_order_relaxed); }
+void fmv_reset_cast_counter(void) { g_casts.store(0, std::memory_order_relaxed); }
+
+int fmv_sbgemv(fmv_ctx* ctx, int mode, char dtype, size_t m, size_t n, size_t batch, size_t lda, size_t stride_a,
+               const void* A, size_t stride_x, const void* x, size_t stride_y, void* y, int force_simple,
+               int* kernel_used) {
+  return guarded([&] {
+    if (!ctx || !A || !x || !y) fail(FMV_EINVAL, "gemv: null argument");
+    if (m == 0 || n == 0 || batch == 0) fail(FMV_EINVAL, "gemv: empty matrix batch");
+    if (lda < m) fail(FMV_EINVAL, "gemv: lda < rows");
+    if (mode < 0 || mode > 2) fail(FMV_EINVAL, "gemv: bad mode");
+    DeviceGuard dg(ctx->device);
+    GemvPlan gp = make_gemv(A, (long)m, (long)n, (long)batch, (long)lda, (long)stride_a, x, (long)stride_x, y,
+                            (long)stride_y);
+    const bool fs = force_simple != 0;
+    switch (dtype) {
+      case 'z': sbgemv_mode<double2, double2>(ctx, mode, gp, fs, kernel_used); break;
+      case 'c': sbgemv_mode<float2, float2>(ctx, mode, gp, fs, kernel_used); break;
+      case 'h': sbgemv_mode<__half2, float2>(ctx, mode, gp, fs, kernel_used); break;
+      case 'd':
+        sbgemv_mode<double, double>(ctx, mode == GM_C ? GM_T : mode, gp, fs, kernel_used);
+        break;
+      case 's':
+        sbgemv_mode<float, float>(ctx, mode == GM_C ? GM_T : mode, gp, fs, kernel_used);
+        break;
+      default: fail(FMV_EINVAL, "gemv: dtype must be s/d/c/z/h");
+    }
+  });
+}
+
+int fmv_comm_unique_id(void* out128) {
+  return guarded([&] {
+    if (!out128) fail(FMV_EINVAL, "null out");
+    nck(nccl().get_unique_id(out128), "ncclGetUniqueId");
+  });
+}
+
+int fmv_comm_init(fmv_ctx* ctx, int nranks, int rank, const void* id128) {
+  return guarded([&] {
+    if (!ctx || nranks < 1 || rank < 0 || rank >= nranks) fail(FMV_EINVAL, "fmv_comm_init: bad arguments");
+    DeviceGuard dg(ctx->device);
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    if (nranks == 1) return;
+    if (!id128) fail(FMV_EINVAL, "fmv_comm_init: null unique id");
+    struct Id {
+      char b[128];
+    } id;
+    std::memcpy(id.b, id128, 128);
+    typedef int (*InitFn)(void**, int, Id, int);
+    auto fn = reinterpret_cast<InitFn>(nccl().comm_init_rank);
+    nck(fn(&ctx->comm, nranks, id, rank), "ncclCommInitRank");
+  });
+}
+
+int fmv_comm_destroy(fmv_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) fail(FMV_EINVAL, "null ctx");
+    if (ctx->comm && nccl().comm_destroy) nccl().comm_destroy(ctx->comm);
+    ctx->comm = nullptr;
+    ctx->nranks = 1;
+    ctx->rank = 0;
+  });
+}
+
+int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* in, double* out,
+                           int io_on_device, fmv_phase_times* times) {
+  return guarded([&] {
+    if (!ctx || !op || !out) fail(FMV_EINVAL, "fmv_matvec_partitioned: null argument");
+    if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
+    const auto p = parse_cfg(cfg);
+    DeviceGuard dg(ctx->device);
+    cudaStream_t s = ctx->stream;
+    const bool fwd = kind == FMV_FORWARD;
+    const size_t nt = op->nt;
+    const size_t n_in = (fwd ? op->nm : op->nd) * nt, n_out = (fwd ? op->nd : op->nm) * nt;
+    auto* te = ctx->te;
+    if (times) CK(cudaEventRecord(te[0], s));
+    const double* din = in;
+    double* dout = out;
+    const bool have_in = fwd || ctx->rank == 0;
+    if (have_in && !in) fail(FMV_EINVAL, "fmv_matvec_partitioned: null input");
+    if (!io_on_device) {
+      ctx->io_in.ensure(std::max(n_in, op->nd * nt) * sizeof(double));
+      ctx->io_out.ensure(n_out * sizeof(double));
+      if (have_in) CK(cudaMemcpyAsync(ctx->io_in.p, in, n_in * sizeof(double), cudaMemcpyHostToDevice, s));
+      din = static_cast<const double*>(ctx->io_in.p);
+      dout = static_cast<double*>(ctx->io_out.p);
+    }
+    if (times) CK(cudaEventRecord(te[1], s));
+    if (fwd) {
+      // partition.hpp:157-182: full-length partial d per rank, summed in cfg[4].
+      pipeline(ctx, op, kind, p, din, -1, dout);
+      if (times) CK(cudaEventRecord(te[2], s));
+      if (ctx->nranks > 1) {
+        const long nd = (long)(op->nd * nt);
+        if (p[4] == PD) {
+          nck(nccl().all_reduce(dout, dout, nd, kNcclDouble, kNcclSum, ctx->comm, s), "ncclAllReduce");
+        } else {
+          ctx->payload.ensure(nd * sizeof(float));
+          float* f = static_cast<float*>(ctx->payload.p);
+          launch(ctx, 4, [&] { k_d2f<<<grid_for(nd, 256, ctx->device), 256, 0, s>>>(dout, f, nd); });
+          nck(nccl().all_reduce(f, f, nd, kNcclFloat, kNcclSum, ctx->comm, s), "ncclAllReduce");
+          launch(ctx, 4, [&] { k_f2d<<<grid_for(nd, 256, ctx->device), 256, 0, s>>>(f, dout, nd); });
+        }
+      }
+      if (times) CK(cudaEventRecord(te[3], s));
+    } else {
+      // partition.hpp:187-217: cast d to cfg[0] once, broadcast, pad from payload.
+      const long nd = (long)(op->nd * nt);
+      const void* pay = din;
+      int pprec = PD;
+      if (p[0] == PD) {
+        if (ctx->nranks > 1) {
+          ctx->payload.ensure(nd * sizeof(double));
+          if (ctx->rank == 0)
+            CK(cudaMemcpyAsync(ctx->payload.p, din, nd * sizeof(double), cudaMemcpyDeviceToDevice, s));
+          nck(nccl().broadcast(ctx->payload.p, ctx->payload.p, nd, kNcclDouble, 0, ctx->comm, s), "ncclBroadcast");
+          pay = ctx->payload.p;
+        }
+      } else {
+        ctx->payload.ensure(nd * sizeof(float));
+        if (ctx->rank == 0) {
+          if (p[0] == PS)
+            launch(ctx, 4, [&] {
+              k_d2f<<<grid_for(nd, 256, ctx->device), 256, 0, s>>>(din, static_cast<float*>(ctx->payload.p), nd);
+            });
+          else
+            launch(ctx, 4, [&] {
+              k_d2h<<<grid_for(nd, 256, ctx->device), 256, 0, s>>>(din, static_cast<__half*>(ctx->payload.p), nd);
+            });
+          g_casts.fetch_add(1, std::memory_order_relaxed);  // partition.hpp:203
+        }
+        if (ctx->nranks > 1)
+          nck(nccl().broadcast(ctx->payload.p, ctx->payload.p, nd, p[0] == PS ? kNcclFloat : kNcclHalf, 0, ctx->comm,
+                               s),
+              "ncclBroadcast");
+        pay = ctx->payload.p;
+        pprec = p[0];
+      }
+      if (times) CK(cudaEventRecord(te[2], s));
+      pipeline(ctx, op, kind, p, pay, pprec, dout);
+      if (times) CK(cudaEventRecord(te[3], s));
+    }
+    if (!io_on_device) CK(cudaMemcpyAsync(out, dout, n_out * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (times) CK(cudaEventRecord(te[4], s));
+    CK(cudaStreamSynchronize(s));
+    if (times) {
+      float a, b, c, d;
+      CK(cudaEventElapsedTime(&a, te[0], te[1]));
+      CK(cudaEventElapsedTime(&b, te[1], te[2]));
+      CK(cudaEventElapsedTime(&c, te[2], te[3]));
+      CK(cudaEventElapsedTime(&d, te[3], te[4]));
+      for (auto& v : times->phase_s) v = 0;
+      if (fwd) {
+        times->phase_s[0] = a * 1e-3;
+        times->phase_s[2] = b * 1e-3;  // whole fused pipeline
+        times->phase_s[4] = (c + d) * 1e-3;  // reduce + copy-out (partition.hpp:178-180)
+      } else {
+        times->phase_s[0] = (a + b) * 1e-3;  // copy-in + broadcast (partition.hpp:204-206)
+        times->phase_s[2] = c * 1e-3;
+        times->phase_s[4] = d * 1e-3;
+      }
+      times->total_s = (a + b + c + d) * 1e-3;
+    }
+  });
+}
+
+}  // extern "C"
