@@ -22,7 +22,7 @@ cpp: build/fftmv_cpp_tests
 
 build/fftmv_cpp_tests: tests/cpp/test_dropin.cpp $(wildcard include/fftmv/*.hpp) include/fftmv_cuda.h $(PKG)/libfftmv_cuda.so
 	@mkdir -p build
-	g++ -std=c++20 -O2 -Wall -Iinclude -o $@ tests/cpp/test_dropin.cpp -L$(PKG) -lfftmv_cuda -Wl,-rpath,'$$ORIGIN/../$(PKG)' -L/usr/local/cuda/lib64 -lcudart
+	g++ -std=c++20 -O2 -Wall -Iinclude -I/usr/local/cuda/include -I$(shell python -c "import sysconfig;print(sysconfig.get_paths()['purelib'])")/include/cudnn_frontend/thirdparty/nlohmann -o $@ tests/cpp/test_dropin.cpp -L$(PKG) -lfftmv_cuda -Wl,-rpath,'$$ORIGIN/../$(PKG)' -L/usr/local/cuda/lib64 -lcudart
 
 clean:
 	rm -f $(PKG)/libfftmv_cuda.so build/fftmv_cpp_tests

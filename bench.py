@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 FFTMatvec hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--cfg ddddd]
+
+One STEP = one forward (d = F m) + one adjoint (m = F* d) matvec on the C2
+operator (Nm=5000, Nd=100, Nt=1000; 8.0 GB of complex128 bins per GPU), so
+the unit of work is one "shard-matvec" over an Nm=5000 column block. At N
+GPUs (torchrun, one rank per GPU) each rank holds its own Nm=5000 shard of an
+Nm=5000*N operator (weak scaling, partition.hpp 1 x p grid): one distributed
+F is N shard-matvecs + an NCCL all-reduce of d, one distributed F* is an NCCL
+broadcast of d + N shard-matvecs.
+
+value   : shard-matvecs/s of the whole job, device-resident inputs (HBM).
+e2e     : the same through the blocking C-ABI call with pinned HOST buffers
+          (H2D of the input and D2H of the output inside the timed region).
+roofline: SBGEMV kernels (the dominant phase, ~90% of a matvec) -- reference
+          algorithmic bytes nb*(Nd*Nm+Nd+Nm)*16 per launch (gemv.hpp:83-89,
+          SURVEY.md §8d) / CUDA-event kernel time, vs MEASURED_PEAKS.json.
+cpu_baseline / --impl reference: the reference itself (oracle/_ref: the
+          reference headers compiled verbatim) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+os.environ.setdefault("MKL_NUM_THREADS", "1")
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+import ctypes  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+SEED = 20250814
+NM, ND, NT = 5000, 100, 1000
+METRIC = "F and F* matvecs/sec at 1/2/4/8 B200; SBGEMV+FFT HBM GB/s vs peak"
+UNIT = "matvecs/s"
+
+
+def env_int(name, dflt):
+    v = os.environ.get(name)
+    return int(v) if v not in (None, "") else dflt
+
+
+def measured_peak_gbs():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the SBGEMV kernels from the committed ncu capture."""
+    p = os.path.join(HERE, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm_, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm_)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_inputs(rank: int):
+    """Synthetic inputs from the reference generators (random_fill.hpp), seeded per shard."""
+    import paper_2508_10202_b200 as F
+
+    base = F.seed_stream(SEED, 1000 + rank) if rank else SEED
+    col = F.uniform_fill(NT * ND * NM, F.seed_stream(base, 0))
+    m = F.uniform_fill(NM * NT, F.seed_stream(base, 1))
+    d = F.uniform_fill(ND * NT, F.seed_stream(SEED, 2))  # d is global (broadcast from rank 0)
+    return col, m, d
+
+
+# ------------------------------------------------------------- reference ---
+def ref_setup(col):
+    from oracle.oracle import ref
+
+    R = ref()
+    t0 = time.time()
+    op = R.setup_operator(NM, ND, NT, col)
+    return R, op, time.time() - t0
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return None
+    col, m, d = make_inputs(0)
+    R, op, t_setup = ref_setup(col)
+    T = cpu_threads()
+    cfg = args.cfg
+    for _ in range(args.warmup):
+        R.throughput_mixed(op, cfg, m, d, T)
+    t = 0.0
+    for _ in range(args.steps):
+        t += R.throughput_mixed(op, cfg, m, d, T)
+    value = args.steps * T / t
+    sample = (f"each step: {T} host threads run concurrently on one shared C2 operator, even threads one F, odd "
+              f"threads one F* (reference forward_matvec/adjoint_matvec, cfg {cfg}); setup_operator {t_setup:.1f}s "
+              f"excluded")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * t / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if cfg == "ddddd" else "mixed", "data": "synthetic",
+        "config": workload_config(world, cfg),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+def workload_config(world, cfg):
+    return {"workload": f"C2 FFTMatvec Nm={NM}/GPU Nd={ND} Nt={NT}, cfg {cfg}, step = 1 F + 1 F*",
+            "n_m_per_gpu": NM, "n_d": ND, "n_t": NT, "n_m_total": NM * world, "precision_config": cfg,
+            "operator_bytes_per_gpu": (NT + 1) * ND * NM * 16,
+            "l2": "inputs larger than L2: the 8.0 GB operator is streamed once per matvec",
+            "parallelism": f"1x{world} column partition" + (" (NCCL all-reduce / broadcast)" if world > 1 else ""),
+            "matvec_unit": "one F or F* over an Nm=5000 shard; a distributed matvec on N GPUs = N units"}
+
+
+# ------------------------------------------------------------------- ours ---
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_2508_10202_b200 as F
+    from paper_2508_10202_b200 import _capi
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # noqa: F811
+
+    col, m_h, d_h = make_inputs(rank)
+    ctx = F.Context(local_rank)
+    op = F.setup_operator(F.BlockColumn(F.ProblemDims(NM, ND, NT), col), ctx)
+    cfg = args.cfg
+    if cfg[2] == "s":
+        op.ensure_single()
+    if cfg[2] == "h":
+        op.ensure_half()
+    L = F.lib()
+    cb = cfg.encode()
+    m = torch.from_numpy(m_h).to(dev)
+    d = torch.from_numpy(d_h).to(dev)
+    dout = torch.empty(ND * NT, dtype=torch.float64, device=dev)
+    mout = torch.empty(NM * NT, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr, device=dev)
+    dm = None
+    if world > 1:
+        dm = F.DistributedMatvec(F.ProblemDims(NM * world, ND, NT), rank, world, shard=op, transport="native", ctx=ctx)
+
+    def step_device():
+        if dm is None:
+            _capi.check(L.fmv_matvec_async(ctx.handle, op.handle, 0, cb, ctypes.c_void_p(m.data_ptr()),
+                                           ctypes.c_void_p(dout.data_ptr())))
+            _capi.check(L.fmv_matvec_async(ctx.handle, op.handle, 1, cb, ctypes.c_void_p(d.data_ptr()),
+                                           ctypes.c_void_p(mout.data_ptr())))
+        else:
+            for kind, x, y in ((0, m, dout), (1, d, mout)):
+                _capi.check(L.fmv_matvec_partitioned(ctx.handle, op.handle, kind, cb, ctypes.c_void_p(x.data_ptr()),
+                                                     ctypes.c_void_p(y.data_ptr()), 1, None))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def timed(fn, k):
+        barrier()
+        ctx.synchronize()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        ctx.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if dist is not None:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    # ---- device-resident throughput (value) + per-kernel CUDA events
+    clk = ClockSampler(local_rank).__enter__()  # samples through warm-up, timed and e2e regions
+    for _ in range(args.warmup):
+        step_device()
+    ctx.synchronize()
+    ctx.set_profiling(True)
+    ctx.profile_read(reset=True)
+    l0 = ctx.launches()
+    ms = timed(step_device, args.steps)
+    launches = ctx.launches() - l0
+    kms, kn = ctx.profile_read(reset=True)
+    ctx.set_profiling(False)
+    value = 2 * args.steps * world / (ms * 1e-3)
+
+    # ---- end to end through the C ABI with pinned host buffers (e2e)
+    m_pin = torch.from_numpy(m_h).pin_memory()
+    d_pin = torch.from_numpy(d_h).pin_memory()
+    do_pin = torch.empty(ND * NT, dtype=torch.float64).pin_memory()
+    mo_pin = torch.empty(NM * NT, dtype=torch.float64).pin_memory()
+
+    def step_host():
+        if dm is None:
+            _capi.check(L.fmv_matvec(ctx.handle, op.handle, 0, cb, ctypes.c_void_p(m_pin.data_ptr()),
+                                     ctypes.c_void_p(do_pin.data_ptr()), 0, None))
+            _capi.check(L.fmv_matvec(ctx.handle, op.handle, 1, cb, ctypes.c_void_p(d_pin.data_ptr()),
+                                     ctypes.c_void_p(mo_pin.data_ptr()), 0, None))
+        else:
+            for kind, x, y in ((0, m_pin, do_pin), (1, d_pin, mo_pin)):
+                _capi.check(L.fmv_matvec_partitioned(ctx.handle, op.handle, kind, cb, ctypes.c_void_p(x.data_ptr()),
+                                                     ctypes.c_void_p(y.data_ptr()), 0, None))
+
+    for _ in range(max(3, args.warmup // 2)):
+        step_host()
+    ms_e2e = timed(step_host, args.steps)
+    clk.__exit__(None, None, None)
+    e2e_value = 2 * args.steps * world / (ms_e2e * 1e-3)
+    h2d = (NM * NT + ND * NT) * 8 * world
+    d2h = (ND * NT + NM * NT) * 8 * world
+
+    # ---- roofline of the dominant kernel (SBGEMV N + C)
+    peak, peak_src = measured_peak_gbs()
+    es = {"d": 16, "s": 8, "h": 4}[cfg[2]]
+    nb = NT + 1
+    gemv_bytes = nb * (ND * NM + ND + NM) * es  # gemv.hpp:83-89 model, per launch
+    n_gemv = kn[1] + kn[2]
+    t_gemv = (kms[1] + kms[2]) * 1e-3
+    achieved = gemv_bytes * n_gemv / t_gemv / 1e9 if t_gemv > 0 else None
+    r2c_bytes = NM * NT * 8 + NM * nb * es  # F's big r2c: real in + TOSI spectrum out
+    c2r_bytes = NM * nb * 16 + NM * NT * 8  # F*'s big c2r
+    detail = {}
+    for name, cls, per in (("sbgemv_n", 1, gemv_bytes), ("sbgemv_c", 2, gemv_bytes)):
+        if kn[cls]:
+            t = kms[cls] / kn[cls] * 1e-3
+            detail[name] = {"ms": t * 1e3, "gbs": per / t / 1e9, "frac": per / t / 1e9 / peak}
+    if kn[0]:
+        detail["r2c_all_ms_per_step"] = kms[0] / args.steps
+    if kn[3]:
+        detail["c2r_all_ms_per_step"] = kms[3] / args.steps
+    detail["fft_big_phase_bytes"] = {"r2c_F": r2c_bytes, "c2r_Fstar": c2r_bytes}
+    share = (kms[1] + kms[2]) / ms if ms > 0 else None
+    traffic = None
+    nc = ncu_traffic()
+    if nc and "sbgemv_dram_bytes_per_launch" in nc:
+        traffic = nc["sbgemv_dram_bytes_per_launch"]
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic, "kernel": "sbgemv (N for F, C for F*)",
+                "algorithmic_bytes_per_launch": gemv_bytes, "peak_source": peak_src, "share_of_step": share,
+                "detail": detail}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if cfg == "ddddd" else f"mixed:{cfg}", "data": "synthetic (reference uniform_fill, seeded)",
+        "config": workload_config(world, cfg),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": ms_e2e / args.steps, "api": "fmv_matvec (C ABI), pinned host buffers"},
+        "gpu_launches": int(launches) * world,
+        "roofline": roofline,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(col, m_h, d_h, cfg)
+    return line
+
+
+def cpu_baseline(col, m, d, cfg):
+    try:
+        R, op, t_setup = ref_setup(col)
+        T = cpu_threads()
+        t = R.throughput_mixed(op, cfg, m, d, T)
+        lat_f = R.throughput(op, 0, cfg, m, 1, 1)
+        return {"value": T / t, "unit": UNIT, "cores": T, "kind": "reference",
+                "sample": (f"{T} threads concurrently, one matvec each (half F, half F*) on one shared C2 operator, "
+                           f"reference headers compiled verbatim (oracle/_ref, FFTW API over MKL DFTI); "
+                           f"1-thread F latency {lat_f:.2f}s; setup_operator {t_setup:.1f}s excluded")}
+    except Exception as e:  # the reference .so is a checker; report why it is missing
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cfg", default="ddddd")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.impl == "reference":
+        line = run_reference_arm(args, rank, world)
+    else:
+        line = run_ours(args, rank, world, local_rank)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1 and args.impl == "ours":
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

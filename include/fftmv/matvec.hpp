@@ -1,0 +1,114 @@
+// matvec.hpp -- drop-in for the reference's five-phase matvec API
+// (matvec.hpp:40-318). The whole pipeline runs in three fused sm_100a
+// kernels inside libfftmv_cuda (fmv_matvec): pad+cast+r2c+reorder,
+// SBGEMV (+ both reorders and casts), reorder+1/L+c2r+unpad+cast.
+// PhaseTimings attribution on B200: [0] H2D of the input, [1] r2c kernel,
+// [2] SBGEMV kernel, [3] c2r kernel, [4] D2H of the output.
+#pragma once
+
+#include <array>
+#include <chrono>
+#include <string>
+#include <complex>
+#include <cstddef>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <utility>
+#include <vector>
+
+#include "fftmv/block_vector.hpp"
+#include "fftmv/config.hpp"
+#include "fftmv/detail_capi.hpp"
+#include "fftmv/gemv.hpp"
+#include "fftmv/operator.hpp"
+
+namespace fftmv {
+
+enum class MatvecKind : std::uint8_t { Forward, Adjoint };
+
+struct PhaseTimings {
+  std::array<double, 5> phase_s{};
+  double total_s = 0.0;
+  PhaseTimings& operator+=(const PhaseTimings& o) {
+    for (std::size_t i = 0; i < 5; ++i) phase_s[i] += o.phase_s[i];
+    total_s += o.total_s;
+    return *this;
+  }
+};
+
+inline const char* phase_name(std::size_t i) {
+  static constexpr const char* kNames[5] = {"pad", "fft", "sbgemv", "ifft", "unpad"};
+  return kNames[i];
+}
+
+struct MatvecResult {
+  BlockVector output;
+  PhaseTimings timings;
+};
+
+namespace detail {
+
+inline double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Working buffer tagged with its precision (the partitioned adjoint's payload).
+struct RealBuf {
+  Precision prec = Precision::Double;
+  std::vector<float> f;
+  std::vector<double> d;
+  std::size_t size() const { return prec == Precision::Double ? d.size() : f.size(); }
+};
+
+inline std::pair<std::vector<double>, PhaseTimings> run_pipeline(const SpectralOperator& op, MatvecKind kind,
+                                                                 std::span<const double> input, const RealBuf* payload,
+                                                                 PrecisionConfig cfg, const TilingParams& = {}) {
+  const bool fwd = kind == MatvecKind::Forward;
+  const std::size_t n_in = (fwd ? op.dims.n_m : op.dims.n_d) * op.dims.n_t;
+  const std::size_t n_out = (fwd ? op.dims.n_d : op.dims.n_m) * op.dims.n_t;
+  std::vector<double> staged;
+  std::string c = cfg.render();
+  if (payload) {
+    // payload already rounded to cfg[0] (partition.hpp:196-206): pad it as is
+    staged = payload->prec == Precision::Double ? payload->d : std::vector<double>(payload->f.begin(), payload->f.end());
+    input = staged;
+    c[0] = 'd';
+  }
+  if (input.size() != n_in) throw std::invalid_argument("matvec: input length does not match operator dims");
+  std::vector<double> out(n_out);
+  fmv_phase_times t{};
+  check(fmv_matvec(thread_ctx(), op.handle(), fwd ? FMV_FORWARD : FMV_ADJOINT, c.c_str(), input.data(), out.data(), 0,
+                   &t));
+  PhaseTimings pt;
+  for (int i = 0; i < 5; ++i) pt.phase_s[i] = t.phase_s[i];
+  pt.total_s = t.total_s;
+  return {std::move(out), pt};
+}
+
+inline void check_matvec_input(const SpectralOperator& op, const BlockVector& v, bool forward) {
+  v.validate();
+  if (v.precision != Precision::Double) throw std::invalid_argument("matvec: input must be double precision");
+  if (v.domain != Domain::Time || v.layout != Layout::SOTI)
+    throw std::invalid_argument("matvec: input must be a time-domain SOTI vector");
+  if (v.space_extent != (forward ? op.dims.n_m : op.dims.n_d) || v.time_extent != op.dims.n_t)
+    throw std::invalid_argument("matvec: input extents do not match operator dims");
+}
+
+}  // namespace detail
+
+inline MatvecResult forward_matvec(const SpectralOperator& op, const BlockVector& m, PrecisionConfig cfg,
+                                   const TilingParams& tiling = {}) {
+  detail::check_matvec_input(op, m, true);
+  auto [out, t] = detail::run_pipeline(op, MatvecKind::Forward, m.f64, nullptr, cfg, tiling);
+  return {BlockVector::time_double(op.dims.n_d, op.dims.n_t, std::move(out)), t};
+}
+
+inline MatvecResult adjoint_matvec(const SpectralOperator& op, const BlockVector& d, PrecisionConfig cfg,
+                                   const TilingParams& tiling = {}) {
+  detail::check_matvec_input(op, d, false);
+  auto [out, t] = detail::run_pipeline(op, MatvecKind::Adjoint, d.f64, nullptr, cfg, tiling);
+  return {BlockVector::time_double(op.dims.n_m, op.dims.n_t, std::move(out)), t};
+}
+
+}  // namespace fftmv

@@ -96,6 +96,14 @@ int fmv_matvec(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const 
 /* Non-blocking variant: device pointers only, enqueued on the ctx stream. */
 int fmv_matvec_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* d_in, double* d_out);
 
+/* ---- batched real FFTs (fft.hpp:110-148), device pointers ----
+ * r2c: batch contiguous series of L reals -> batch x (L/2+1) complex bins,
+ *      unnormalized, sign -1. c2r: the true inverse, 1/L folded in by
+ *      pre-scaling in the working precision. prec 'd' (double/complex double)
+ *      or 's' (float/complex float). L must be even and >= 2. */
+int fmv_fft_r2c(fmv_ctx* ctx, size_t L, size_t batch, char prec, const void* d_in, void* d_out);
+int fmv_fft_c2r(fmv_ctx* ctx, size_t L, size_t batch, char prec, const void* d_in, void* d_out);
+
 /* ---- casts (precision.hpp:27-39): logical conversion passes performed ---- */
 uint64_t fmv_casts_performed(void);
 void fmv_reset_cast_counter(void);

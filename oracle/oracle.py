@@ -160,6 +160,7 @@ class Ref(_Base):
         self._f("pareto", c_int, [c_size_t, c_void_p, c_void_p, c_char_p, c_void_p])
         self._f("optimal", c_int, [c_size_t, c_void_p, c_void_p, c_char_p, c_double, c_void_p])
         self._f("throughput", c_int, [c_void_p, c_int, c_char_p, c_void_p, c_int, c_int, POINTER(c_double)])
+        self._f("throughput_mixed", c_int, [c_void_p, c_char_p, c_void_p, c_void_p, c_int, POINTER(c_double)])
         self._f("op_materialize_single", None, [c_void_p])
         self._f("effective_bandwidth", c_int, [c_size_t, c_size_t, c_size_t, c_size_t, c_double, POINTER(c_double)])
         self._f("select_kernel", c_int, [c_size_t, c_size_t, c_int, c_size_t, c_size_t, c_double, c_size_t])
@@ -186,6 +187,14 @@ class Ref(_Base):
         x = np.ascontiguousarray(x, dtype=np.float64)
         s = c_double()
         if self._throughput(op.h, kind, cfg.encode(), x.ctypes.data, threads, per_thread, ctypes.byref(s)):
+            raise RuntimeError(self.err())
+        return s.value
+
+    def throughput_mixed(self, op, cfg, m, d, threads):
+        m = np.ascontiguousarray(m, dtype=np.float64)
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        s = c_double()
+        if self._throughput_mixed(op.h, cfg.encode(), m.ctypes.data, d.ctypes.data, threads, ctypes.byref(s)):
             raise RuntimeError(self.err())
         return s.value
 

@@ -365,4 +365,34 @@ int ref_throughput(void* op, int kind, const char* cfg, const double* in, int th
   });
 }
 
+// CPU reference arm: `threads` std::threads run concurrently on the shared
+// operator, even-numbered threads one forward matvec each, odd-numbered one
+// adjoint matvec each. Wall seconds of the whole batch.
+int ref_throughput_mixed(void* op, const char* cfg, const double* m, const double* d, int threads, double* seconds) {
+  return guarded([&] {
+    const auto* o = static_cast<SpectralOperator*>(op);
+    const auto c = parse_precision_config(cfg);
+    materialize_single(*o);
+    const auto vm = BlockVector::time_double(o->dims.n_m, o->dims.n_t, std::vector<double>(m, m + o->dims.n_m * o->dims.n_t));
+    const auto vd = BlockVector::time_double(o->dims.n_d, o->dims.n_t, std::vector<double>(d, d + o->dims.n_d * o->dims.n_t));
+    std::atomic<int> failures{0};
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t)
+      pool.emplace_back([&, t] {
+        try {
+          if (t % 2 == 0)
+            (void)forward_matvec(*o, vm, c);
+          else
+            (void)adjoint_matvec(*o, vd, c);
+        } catch (...) {
+          failures.fetch_add(1);
+        }
+      });
+    for (auto& th : pool) th.join();
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (failures.load()) throw std::runtime_error("ref_throughput_mixed: a worker thread failed");
+  });
+}
+
 }  // extern "C"

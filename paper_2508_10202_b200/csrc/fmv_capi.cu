@@ -370,11 +370,11 @@ int fft_series_per_cta(int N, size_t celem) {
 }
 
 template <int C0, int C1, int C2, class Tin>
-void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, int Nt, void* out, long out_ks,
-           long out_ss) {
+void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, int N, int nvalid, void* out,
+           long out_ks, long out_ss) {
   using R = typename PT<C1>::real;
   using C = typename CT<R>::c;
-  const FftGeom g = make_geom(Nt);
+  const FftGeom g = make_geom(N);
   const int S = fft_series_per_cta(g.N, sizeof(C));
   const size_t smem = 2 * (size_t)S * (g.N + 1) * sizeof(C);
   auto kern = k_r2c<C0, C1, C2, Tin>;
@@ -382,18 +382,20 @@ void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, in
   const C* tw = static_cast<const C*>(twiddles().get(ctx->device, g.L, C1));
   const long grid = (nseries + S - 1) / S;
   launch(ctx, 0, [&] {
-    kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(in, in_ss, in_ts, nseries, Nt,
+    kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(in, in_ss, in_ts, nseries, nvalid,
                                                      static_cast<typename PT<C2>::cplx*>(out), out_ks, out_ss, g, tw, S);
   });
 }
 
+// N = L/2 (complex FFT length); nvalid = input samples per series (Nt for
+// the zero-padded matvec path, L for a plain transform).
 template <class Tin>
-void r2c_dispatch(fmv_ctx* ctx, int c0, int c1, int c2, const Tin* in, long in_ss, long in_ts, long nseries, int Nt,
-                  void* out, long out_ks, long out_ss) {
-#define R2C_CASE(A, B, C)                                                                 \
-  if (c0 == A && c1 == B && c2 == C) {                                                    \
-    r2c_t<A, B, C, Tin>(ctx, in, in_ss, in_ts, nseries, Nt, out, out_ks, out_ss);         \
-    return;                                                                               \
+void r2c_dispatch(fmv_ctx* ctx, int c0, int c1, int c2, const Tin* in, long in_ss, long in_ts, long nseries, int N,
+                  int nvalid, void* out, long out_ks, long out_ss) {
+#define R2C_CASE(A, B, C)                                                                      \
+  if (c0 == A && c1 == B && c2 == C) {                                                         \
+    r2c_t<A, B, C, Tin>(ctx, in, in_ss, in_ts, nseries, N, nvalid, out, out_ks, out_ss);       \
+    return;                                                                                    \
   }
   R2C_CASE(PD, PD, PD) R2C_CASE(PD, PD, PS) R2C_CASE(PD, PD, PH)
   R2C_CASE(PD, PS, PD) R2C_CASE(PD, PS, PS) R2C_CASE(PD, PS, PH)
@@ -405,28 +407,29 @@ void r2c_dispatch(fmv_ctx* ctx, int c0, int c1, int c2, const Tin* in, long in_s
   fail(FMV_EINVAL, "r2c: unsupported precision combination");
 }
 
-template <int C3, int C4>
-void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, int Nt, double* out, long out_ss) {
+template <int C3, int C4, class Tout>
+void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, int N, int nout, Tout* out,
+           long out_ss) {
   using C = typename PT<C3>::cplx;
-  const FftGeom g = make_geom(Nt);
+  const FftGeom g = make_geom(N);
   const int S = fft_series_per_cta(g.N, sizeof(C));
   const size_t smem = 2 * (size_t)S * (g.N + 1) * sizeof(C);
-  auto kern = k_c2r<C3, C4>;
+  auto kern = k_c2r<C3, C4, Tout>;
   prep_smem((const void*)kern, smem);
   const C* tw = static_cast<const C*>(twiddles().get(ctx->device, g.L, C3));
   const long grid = (nseries + S - 1) / S;
   launch(ctx, 3, [&] {
-    kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(static_cast<const C*>(in), in_ks, in_ss, nseries, Nt, out,
+    kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(static_cast<const C*>(in), in_ks, in_ss, nseries, nout, out,
                                                      out_ss, g, tw, S);
   });
 }
 
-void c2r_dispatch(fmv_ctx* ctx, int c3, int c4, const void* in, long in_ks, long in_ss, long nseries, int Nt,
-                  double* out, long out_ss) {
-#define C2R_CASE(A, B)                                                  \
-  if (c3 == A && c4 == B) {                                             \
-    c2r_t<A, B>(ctx, in, in_ks, in_ss, nseries, Nt, out, out_ss);       \
-    return;                                                             \
+void c2r_dispatch(fmv_ctx* ctx, int c3, int c4, const void* in, long in_ks, long in_ss, long nseries, int N,
+                  int nout, double* out, long out_ss) {
+#define C2R_CASE(A, B)                                                              \
+  if (c3 == A && c4 == B) {                                                         \
+    c2r_t<A, B, double>(ctx, in, in_ks, in_ss, nseries, N, nout, out, out_ss);      \
+    return;                                                                         \
   }
   C2R_CASE(PD, PD) C2R_CASE(PD, PS) C2R_CASE(PD, PH) C2R_CASE(PS, PD) C2R_CASE(PS, PS) C2R_CASE(PS, PH)
 #undef C2R_CASE
@@ -585,13 +588,17 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
   ctx->y.ensure((size_t)nb * n_out * e3 + 256);
   // Phases 1-2 (+ reorder to TOSI, cast to cfg[2]).
   if (payload_prec < 0)
-    r2c_dispatch<double>(ctx, p[0], p[1], p[2], static_cast<const double*>(in), nt, 1, n_in, (int)nt, ctx->x.p, n_in, 1);
+    r2c_dispatch<double>(ctx, p[0], p[1], p[2], static_cast<const double*>(in), nt, 1, n_in, (int)nt, (int)nt,
+                         ctx->x.p, n_in, 1);
   else if (payload_prec == PD)
-    r2c_dispatch<double>(ctx, PD, p[1], p[2], static_cast<const double*>(in), nt, 1, n_in, (int)nt, ctx->x.p, n_in, 1);
+    r2c_dispatch<double>(ctx, PD, p[1], p[2], static_cast<const double*>(in), nt, 1, n_in, (int)nt, (int)nt,
+                         ctx->x.p, n_in, 1);
   else if (payload_prec == PS)
-    r2c_dispatch<float>(ctx, PS, p[1], p[2], static_cast<const float*>(in), nt, 1, n_in, (int)nt, ctx->x.p, n_in, 1);
+    r2c_dispatch<float>(ctx, PS, p[1], p[2], static_cast<const float*>(in), nt, 1, n_in, (int)nt, (int)nt, ctx->x.p,
+                        n_in, 1);
   else
-    r2c_dispatch<__half>(ctx, PH, p[1], p[2], static_cast<const __half*>(in), nt, 1, n_in, (int)nt, ctx->x.p, n_in, 1);
+    r2c_dispatch<__half>(ctx, PH, p[1], p[2], static_cast<const __half*>(in), nt, 1, n_in, (int)nt, (int)nt,
+                         ctx->x.p, n_in, 1);
   if (ev_r2c) CK(cudaEventRecord(ev_r2c, ctx->stream));
   // Phase 3 SBGEMV in cfg[2], output cast to cfg[3], TOSI.
   const long m = (long)op->nd, n = (long)op->nm;
@@ -610,7 +617,7 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
   }
   if (ev_gemv) CK(cudaEventRecord(ev_gemv, ctx->stream));
   // Phases 4-5 (+ reorder back to SOTI, 1/L in cfg[3], unpad, cast cfg[4]).
-  c2r_dispatch(ctx, p[3], p[4], ctx->y.p, n_out, 1, n_out, (int)nt, out, nt);
+  c2r_dispatch(ctx, p[3], p[4], ctx->y.p, n_out, 1, n_out, (int)nt, (int)nt, out, nt);
   g_casts.fetch_add(count_casts(p, payload_prec >= 0), std::memory_order_relaxed);
 }
 
@@ -814,7 +821,7 @@ int fmv_op_create(fmv_ctx* ctx, size_t nm, size_t nd, size_t nt, const double* c
     }
     // operator.hpp:99-125: every (i,j) series, time-outer in the column,
     // padded to 2nt and r2c'd in fp64, written bin-major.
-    r2c_dispatch<double>(ctx, PD, PD, PD, dcol, 1, (long)S, (long)S, (int)nt, op->bins_d, (long)S, 1);
+    r2c_dispatch<double>(ctx, PD, PD, PD, dcol, 1, (long)S, (long)S, (int)nt, (int)nt, op->bins_d, (long)S, 1);
     CK(cudaStreamSynchronize(ctx->stream));
     if (tmp) cudaFree(tmp);
     *out = op.release();
@@ -936,6 +943,40 @@ int fmv_matvec(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const 
       }
       times->total_s = tot;
     }
+  });
+}
+
+int fmv_fft_r2c(fmv_ctx* ctx, size_t L, size_t batch, char prec, const void* d_in, void* d_out) {
+  return guarded([&] {
+    if (!ctx || !d_in || !d_out) fail(FMV_EINVAL, "fft: null argument");
+    if (L < 2 || L % 2) fail(FMV_EINVAL, "FftPlan: length must be even and >= 2");
+    if (batch < 1) fail(FMV_EINVAL, "FftPlan: batch must be >= 1");
+    DeviceGuard dg(ctx->device);
+    const long nb = (long)L / 2 + 1;
+    if (prec == 'd')
+      r2c_t<PD, PD, PD, double>(ctx, static_cast<const double*>(d_in), (long)L, 1, (long)batch, (int)L / 2, (int)L,
+                                d_out, 1, nb);
+    else if (prec == 's')
+      r2c_t<PS, PS, PS, float>(ctx, static_cast<const float*>(d_in), (long)L, 1, (long)batch, (int)L / 2, (int)L,
+                               d_out, 1, nb);
+    else
+      fail(FMV_EINVAL, "fft: prec must be 'd' or 's'");
+  });
+}
+
+int fmv_fft_c2r(fmv_ctx* ctx, size_t L, size_t batch, char prec, const void* d_in, void* d_out) {
+  return guarded([&] {
+    if (!ctx || !d_in || !d_out) fail(FMV_EINVAL, "fft: null argument");
+    if (L < 2 || L % 2) fail(FMV_EINVAL, "FftPlan: length must be even and >= 2");
+    if (batch < 1) fail(FMV_EINVAL, "FftPlan: batch must be >= 1");
+    DeviceGuard dg(ctx->device);
+    const long nb = (long)L / 2 + 1;
+    if (prec == 'd')
+      c2r_t<PD, PD, double>(ctx, d_in, 1, nb, (long)batch, (int)L / 2, (int)L, static_cast<double*>(d_out), (long)L);
+    else if (prec == 's')
+      c2r_t<PS, PS, float>(ctx, d_in, 1, nb, (long)batch, (int)L / 2, (int)L, static_cast<float*>(d_out), (long)L);
+    else
+      fail(FMV_EINVAL, "fft: prec must be 'd' or 's'");
   });
 }
 

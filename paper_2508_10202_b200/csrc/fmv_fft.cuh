@@ -198,13 +198,13 @@ __device__ typename CT<R>::c* run_stages(typename CT<R>::c* a, typename CT<R>::c
 }
 
 // Phases 1-2 (+ the SOTI->TOSI reorder of phase 3), fused:
-//   v = rnd_C1(rnd_C0(in[s, t])) for t < Nt, 0 for Nt <= t < L   (matvec.hpp:84-90, :118-130)
+//   v = rnd_C1(rnd_C0(in[s, t])) for t < nvalid (= Nt), 0 up to L  (matvec.hpp:84-90, :118-130)
 //   X = r2c_L(v) in C1 arithmetic                                  (matvec.hpp:132-141)
 //   out[k, s] = rnd_C2(X[k])                                       (matvec.hpp:155-165)
 // Input element (s,t) at in[s*in_ss + t*in_ts]; output bin k of series s at
 // out[k*out_ks + s*out_ss]. One CTA per S consecutive series.
 template <int C0, int C1, int C2, class Tin>
-__global__ void __launch_bounds__(256) k_r2c(const Tin* __restrict__ in, long in_ss, long in_ts, long nseries, int Nt,
+__global__ void __launch_bounds__(256) k_r2c(const Tin* __restrict__ in, long in_ss, long in_ts, long nseries, int nvalid,
                                              typename PT<C2>::cplx* __restrict__ out, long out_ks, long out_ss,
                                              FftGeom g, const typename CT<typename PT<C1>::real>::c* __restrict__ tw,
                                              int S) {
@@ -224,8 +224,8 @@ __global__ void __launch_bounds__(256) k_r2c(const Tin* __restrict__ in, long in
       const int s = e / N, n = e - s * N;
       const Tin* p = in + (s0 + s) * in_ss;
       const int t0 = 2 * n, t1 = 2 * n + 1;
-      const R a = t0 < Nt ? (R)rnd<C0>(to_d(p[t0])) : R(0);
-      const R b = t1 < Nt ? (R)rnd<C0>(to_d(p[t1])) : R(0);
+      const R a = t0 < nvalid ? (R)rnd<C0>(to_d(p[t0])) : R(0);
+      const R b = t1 < nvalid ? (R)rnd<C0>(to_d(p[t1])) : R(0);
       bufA[s * ss + n] = C{a, b};
     }
   } else {
@@ -233,8 +233,8 @@ __global__ void __launch_bounds__(256) k_r2c(const Tin* __restrict__ in, long in
       const int n = e / ns, s = e - n * ns;
       const Tin* p = in + (s0 + s) * in_ss;
       const int t0 = 2 * n, t1 = 2 * n + 1;
-      const R a = t0 < Nt ? (R)rnd<C0>(to_d(p[(long)t0 * in_ts])) : R(0);
-      const R b = t1 < Nt ? (R)rnd<C0>(to_d(p[(long)t1 * in_ts])) : R(0);
+      const R a = t0 < nvalid ? (R)rnd<C0>(to_d(p[(long)t0 * in_ts])) : R(0);
+      const R b = t1 < nvalid ? (R)rnd<C0>(to_d(p[(long)t1 * in_ts])) : R(0);
       bufA[s * ss + n] = C{a, b};
     }
   }
@@ -265,10 +265,10 @@ __global__ void __launch_bounds__(256) k_r2c(const Tin* __restrict__ in, long in
 // Phases 4-5 (+ the TOSI->SOTI reorder of phase 3), fused:
 //   Xs = in[k, s] * (1/L) in C3 arithmetic, Im(X0)=Im(XN)=0        (fft.hpp:130-148)
 //   x = c2r_L(Xs) in C3 arithmetic
-//   out[s, t] = (double) rnd_C4(x[t]), t < Nt                      (matvec.hpp:184-192)
-template <int C3, int C4>
+//   out[s, t] = (double) rnd_C4(x[t]), t < nout (= Nt)             (matvec.hpp:184-192)
+template <int C3, int C4, class Tout>
 __global__ void __launch_bounds__(256) k_c2r(const typename PT<C3>::cplx* __restrict__ in, long in_ks, long in_ss,
-                                             long nseries, int Nt, double* __restrict__ out, long out_ss, FftGeom g,
+                                             long nseries, int nout, Tout* __restrict__ out, long out_ss, FftGeom g,
                                              const typename PT<C3>::cplx* __restrict__ tw, int S) {
   using R = typename PT<C3>::real;
   using C = typename CT<R>::c;
@@ -307,10 +307,10 @@ __global__ void __launch_bounds__(256) k_c2r(const typename PT<C3>::cplx* __rest
   }
   __syncthreads();
   const C* z = run_stages<R, 1>(bufB, bufA, ss, ns, g, tw);
-  for (int e = threadIdx.x; e < ns * Nt; e += blockDim.x) {
-    const int s = e / Nt, t = e - s * Nt;
+  for (int e = threadIdx.x; e < ns * nout; e += blockDim.x) {
+    const int s = e / nout, t = e - s * nout;
     const C v = z[s * ss + (t >> 1)];
-    out[(s0 + s) * out_ss + t] = rnd<C4>((double)((t & 1) ? v.y : v.x));
+    out[(s0 + s) * out_ss + t] = (Tout)rnd<C4>((double)((t & 1) ? v.y : v.x));
   }
 }
 

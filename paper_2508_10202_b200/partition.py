@@ -1,0 +1,288 @@
+"""1 x p column partition of the operator (partition.hpp:19-238).
+
+Two execution modes:
+
+* In-process (reference semantics, partition.hpp:1-8): every shard is its
+  own SpectralOperator on one GPU, shards run one after another and the
+  forward partials meet in the reference's fixed left-balanced tree in cfg[4]
+  precision. Used for parity with the reference's simulated partition.
+* Distributed (the B200 deployment): one process per GPU. Each rank holds
+  its shard's operator; the forward partial d is summed with an NCCL
+  all-reduce in cfg[4] precision and the adjoint input is broadcast in cfg[0]
+  precision, both issued from inside libfftmv_cuda (fmv_matvec_partitioned)
+  on the matvec's own stream. A torch.distributed transport (gloo on CPU,
+  nccl on GPU) with an injectable per-shard compute covers the same host
+  logic in CPU tests.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional
+
+import numpy as np
+
+from . import _capi
+from ._capi import check, lib
+from .fftmv import (BlockColumn, BlockVector, Context, Domain, Layout, MatvecKind, PhaseTimings, Precision,
+                    PrecisionConfig, ProblemDims, SpectralOperator, _cfg_str, _is_cuda_tensor, default_context,
+                    run_pipeline, setup_operator)
+
+__all__ = ["Grid1xP", "CommSpec", "shard_operator", "tree_reduce", "PartitionedOperator", "PartitionedResult",
+           "setup_partitioned", "forward_matvec_partitioned", "adjoint_matvec_partitioned", "round_to",
+           "DistributedMatvec"]
+
+
+@dataclass
+class Grid1xP:
+    """partition.hpp:23-43: balanced contiguous Nm ranges, leading ranges take the remainder."""
+
+    p: int = 1
+    shard_ranges: List[tuple] = field(default_factory=list)
+
+    @staticmethod
+    def split(p: int, n_m: int) -> "Grid1xP":
+        if p < 1:
+            raise ValueError("Grid1xP: p must be >= 1")
+        if p > n_m:
+            raise ValueError("Grid1xP: more workers than parameter columns")
+        base, rem = divmod(n_m, p)
+        ranges, begin = [], 0
+        for w in range(p):
+            size = base + (1 if w < rem else 0)
+            ranges.append((begin, begin + size))
+            begin += size
+        return Grid1xP(p, ranges)
+
+    def shard_size(self, w: int) -> int:
+        return self.shard_ranges[w][1] - self.shard_ranges[w][0]
+
+
+@dataclass
+class CommSpec:
+    """partition.hpp:47-59: both collectives move n_d * n_t values."""
+
+    class Op(enum.IntEnum):
+        Reduce = 0
+        Broadcast = 1
+
+    op: "CommSpec.Op"
+    precision: Precision
+    buffer_len: int
+
+    @staticmethod
+    def forward_reduce(cfg: PrecisionConfig, dims: ProblemDims) -> "CommSpec":
+        return CommSpec(CommSpec.Op.Reduce, cfg[4], dims.n_d * dims.n_t)
+
+    @staticmethod
+    def adjoint_broadcast(cfg: PrecisionConfig, dims: ProblemDims) -> "CommSpec":
+        return CommSpec(CommSpec.Op.Broadcast, cfg[0], dims.n_d * dims.n_t)
+
+
+def shard_operator(col: BlockColumn, grid: Grid1xP) -> List[BlockColumn]:
+    """partition.hpp:63-80: worker w gets columns [lo, hi) of every block."""
+    d = col.dims
+    if not grid.shard_ranges or grid.shard_ranges[-1][1] != d.n_m:
+        raise ValueError("shard_operator: grid does not cover n_m")
+    blocks = np.asarray(col.data).reshape(d.n_t, d.n_m, d.n_d)  # [t][j][i] (column-major blocks)
+    out = []
+    for lo, hi in grid.shard_ranges:
+        out.append(BlockColumn(ProblemDims(hi - lo, d.n_d, d.n_t), np.ascontiguousarray(blocks[:, lo:hi, :]).reshape(-1)))
+    return out
+
+
+def round_to(x: np.ndarray, p: str) -> np.ndarray:
+    """Value rounding to a phase precision (precision.hpp:44-61; 'h' = fp16 ext.)."""
+    if p == "s":
+        return np.asarray(x, dtype=np.float64).astype(np.float32).astype(np.float64)
+    if p == "h":
+        return np.asarray(x, dtype=np.float64).astype(np.float16).astype(np.float64)
+    return np.asarray(x, dtype=np.float64)
+
+
+def tree_reduce(buffers: List[np.ndarray], precision: Precision) -> np.ndarray:
+    """partition.hpp:84-132: inputs cast to `precision`, fixed left-balanced
+    pairwise tree ((b0+b1)+(b2+b3)), ((b0+b1)+b2) for odd counts, root -> double."""
+    if not buffers:
+        raise ValueError("tree_reduce: no buffers")
+    n = len(buffers[0])
+    dt = np.float64 if precision == Precision.Double else np.float32
+    level = []
+    for b in buffers:
+        if len(b) != n:
+            raise ValueError("tree_reduce: buffer length mismatch")
+        level.append(np.asarray(b, dtype=np.float64).astype(dt))
+    while len(level) > 1:
+        nxt = [level[k] + level[k + 1] for k in range(0, len(level) - 1, 2)]
+        if len(level) % 2 == 1:
+            nxt.append(level[-1])
+        level = nxt
+    return level[0].astype(np.float64)
+
+
+# ---------------------------------------------------- in-process (simulated) ---
+@dataclass
+class PartitionedOperator:
+    """partition.hpp:135-147."""
+
+    dims: ProblemDims
+    grid: Grid1xP
+    workers: List[SpectralOperator]
+
+
+@dataclass
+class PartitionedResult:
+    output: BlockVector
+    timings: PhaseTimings
+
+
+def setup_partitioned(col: BlockColumn, grid: Grid1xP, ctx: Optional[Context] = None) -> PartitionedOperator:
+    return PartitionedOperator(col.dims, grid, [setup_operator(s, ctx) for s in shard_operator(col, grid)])
+
+
+def _payload_cfg(cfg: str) -> str:
+    # The broadcast payload is already rounded to cfg[0] (partition.hpp:198-203);
+    # padding it again is exact, so the shard pipeline runs with slot 0 = 'd'.
+    return "d" + cfg[1:]
+
+
+def forward_matvec_partitioned(pop: PartitionedOperator, m, cfg="ddddd") -> PartitionedResult:
+    """partition.hpp:157-182 (restated: the reference's own check at :159
+    rejects every p >= 2)."""
+    c = _cfg_str(cfg)
+    m = np.ascontiguousarray(m.data if isinstance(m, BlockVector) else m, dtype=np.float64).reshape(-1)
+    nt = pop.dims.n_t
+    if m.size != pop.dims.n_m * nt:
+        raise ValueError("partitioned matvec: input extents do not match dims")
+    total = PhaseTimings()
+    partials = []
+    for (lo, hi), op in zip(pop.grid.shard_ranges, pop.workers):
+        part, t = run_pipeline(op, MatvecKind.Forward, m[lo * nt:hi * nt], c)
+        total += t
+        partials.append(part)
+    d = tree_reduce(partials, Precision.Double if c[4] == "d" else Precision.Single)
+    return PartitionedResult(BlockVector.time_double(pop.dims.n_d, nt, d), total)
+
+
+def adjoint_matvec_partitioned(pop: PartitionedOperator, d, cfg="ddddd") -> PartitionedResult:
+    """partition.hpp:187-217: cast d to cfg[0] once, every shard pads from that payload."""
+    c = _cfg_str(cfg)
+    d = np.ascontiguousarray(d.data if isinstance(d, BlockVector) else d, dtype=np.float64).reshape(-1)
+    nt = pop.dims.n_t
+    if d.size != pop.dims.n_d * nt:
+        raise ValueError("partitioned matvec: input extents do not match dims")
+    payload = round_to(d, c[0])
+    total = PhaseTimings()
+    out = np.empty(pop.dims.n_m * nt)
+    for (lo, hi), op in zip(pop.grid.shard_ranges, pop.workers):
+        shard, t = run_pipeline(op, MatvecKind.Adjoint, payload, _payload_cfg(c))
+        total += t
+        out[lo * nt:hi * nt] = shard
+    return PartitionedResult(BlockVector.time_double(pop.dims.n_m, nt, out), total)
+
+
+# ------------------------------------------------------------ distributed ---
+class DistributedMatvec:
+    """One rank of a 1 x p partitioned operator.
+
+    transport="native": NCCL inside libfftmv_cuda (fmv_comm_init +
+      fmv_matvec_partitioned); requires torch.distributed to be initialised
+      (used only to ship rank 0's NCCL unique id).
+    transport="torch": collectives through torch.distributed (gloo or nccl)
+      on host arrays, compute through ``compute(kind, cfg, x) -> np.ndarray``
+      (default: this rank's GPU shard via run_pipeline). Lets the host logic
+      run with world_size > 1 on CPU.
+    """
+
+    def __init__(self, dims: ProblemDims, rank: int, world: int, shard: Optional[SpectralOperator] = None,
+                 transport: str = "native", compute: Optional[Callable] = None, ctx: Optional[Context] = None):
+        self.dims = dims
+        self.rank = rank
+        self.world = world
+        self.grid = Grid1xP.split(world, dims.n_m)
+        self.lo, self.hi = self.grid.shard_ranges[rank]
+        self.shard = shard
+        self.transport = transport
+        self.ctx = ctx or (shard.ctx if shard is not None else None)
+        if transport == "native":
+            if shard is None:
+                raise ValueError("native transport needs the rank's SpectralOperator shard")
+            self._init_native()
+        elif transport == "torch":
+            self.compute = compute or (lambda kind, cfg, x: run_pipeline(self.shard, kind, x, cfg)[0])
+        else:
+            raise ValueError("transport must be 'native' or 'torch'")
+
+    def _init_native(self):
+        import torch.distributed as dist
+
+        idb = (ctypes.c_char * 128)()
+        if self.world > 1:
+            if self.rank == 0:
+                check(lib().fmv_comm_unique_id(idb))
+            obj = [bytes(idb)] if self.rank == 0 else [None]
+            dist.broadcast_object_list(obj, src=0)
+            idb = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+        check(lib().fmv_comm_init(self.ctx.handle, self.world, self.rank, idb))
+
+    # -- forward: local slice in, full d out on every rank
+    def forward(self, m_slice, cfg="ddddd", times: bool = False):
+        c = _cfg_str(cfg)
+        nt = self.dims.n_t
+        if self.transport == "native":
+            return self._native(MatvecKind.Forward, c, m_slice, self.dims.n_d * nt, times)
+        import torch
+        import torch.distributed as dist
+
+        part = np.asarray(self.compute(MatvecKind.Forward, c, np.ascontiguousarray(m_slice, dtype=np.float64)))
+        if self.world == 1:
+            return part
+        t = torch.from_numpy(part.astype(np.float64 if c[4] == "d" else np.float32))
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return t.numpy().astype(np.float64)
+
+    # -- adjoint: full d (rank 0) in, local m slice out
+    def adjoint(self, d_full, cfg="ddddd", times: bool = False):
+        c = _cfg_str(cfg)
+        nt = self.dims.n_t
+        n_slice = (self.hi - self.lo) * nt
+        if self.transport == "native":
+            return self._native(MatvecKind.Adjoint, c, d_full, n_slice, times)
+        import torch
+        import torch.distributed as dist
+
+        nd = self.dims.n_d * nt
+        bdt = {"d": np.float64, "s": np.float32, "h": np.float16}[c[0]]
+        buf = np.zeros(nd, dtype=bdt)
+        if self.rank == 0:
+            buf[:] = np.asarray(d_full, dtype=np.float64).astype(bdt)
+        t = torch.from_numpy(buf)
+        if self.world > 1:
+            dist.broadcast(t, src=0)
+        payload = t.numpy().astype(np.float64)
+        return np.asarray(self.compute(MatvecKind.Adjoint, _payload_cfg(c), payload))
+
+    def _native(self, kind, c, x, n_out, times):
+        t = _capi.PhaseTimesC()
+        if _is_cuda_tensor(x):
+            import torch
+
+            out = torch.empty(n_out, dtype=torch.float64, device=x.device)
+            torch.cuda.current_stream(x.device).synchronize()
+            check(lib().fmv_matvec_partitioned(self.ctx.handle, self.shard.handle, int(kind), c.encode(),
+                                               ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), 1,
+                                               ctypes.byref(t)))
+        else:
+            out = np.empty(n_out)
+            xin = None if x is None else np.ascontiguousarray(x, dtype=np.float64)
+            check(lib().fmv_matvec_partitioned(self.ctx.handle, self.shard.handle, int(kind), c.encode(),
+                                               None if xin is None else xin.ctypes.data, out.ctypes.data, 0,
+                                               ctypes.byref(t)))
+        if times:
+            return out, PhaseTimings(list(t.phase_s), t.total_s)
+        return out
+
+    def close(self):
+        if self.transport == "native" and self.ctx is not None:
+            lib().fmv_comm_destroy(self.ctx.handle)

@@ -1,0 +1,150 @@
+// Drop-in check: code written against the reference API (namespace fftmv,
+// reference headers' names and signatures) compiles unchanged against
+// include/fftmv/*.hpp and runs on the B200 kernels.
+//   build/fftmv_cpp_tests          host-only checks (no GPU needed)
+//   build/fftmv_cpp_tests --gpu    + operator setup / matvecs / partition / sweep on cuda:0
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fftmv/block_vector.hpp"
+#include "fftmv/config.hpp"
+#include "fftmv/dims.hpp"
+#include "fftmv/fft.hpp"
+#include "fftmv/gemv.hpp"
+#include "fftmv/matvec.hpp"
+#include "fftmv/operator.hpp"
+#include "fftmv/partition.hpp"
+#include "fftmv/random_fill.hpp"
+#include "fftmv/sweep.hpp"
+
+using namespace fftmv;
+
+static int failures = 0;
+#define EXPECT(c)                                                          \
+  do {                                                                     \
+    if (!(c)) {                                                            \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);             \
+      ++failures;                                                          \
+    }                                                                      \
+  } while (0)
+
+template <class F>
+static bool throws_invalid(F&& f) {
+  try {
+    f();
+  } catch (const std::invalid_argument&) {
+    return true;
+  }
+  return false;
+}
+
+static void host_checks() {
+  EXPECT(throws_invalid([] { ProblemDims(0, 1, 1); }));
+  EXPECT(ProblemDims(5, 3, 7).fft_len() == 14 && ProblemDims(5, 3, 7).n_bins() == 8);
+  EXPECT(parse_precision_config("dssdd").render() == "dssdd");
+  EXPECT(throws_invalid([] { parse_precision_config("dsxdd"); }));
+  EXPECT(throws_invalid([] { parse_precision_config("dss"); }));
+  auto all = enumerate_configs();
+  EXPECT(all.size() == 32 && all.front().render() == "ddddd" && all.back().render() == "sssss");
+  EXPECT(all[1].render() == "dddds");
+  auto g = Grid1xP::split(3, 5);
+  EXPECT(g.shard_size(0) == 2 && g.shard_size(1) == 2 && g.shard_size(2) == 1);
+  EXPECT(throws_invalid([] { Grid1xP::split(6, 5); }));
+  std::vector<std::vector<double>> b = {{1}, {2}, {3}, {4}};
+  EXPECT(tree_reduce(b, Precision::Double)[0] == 10.0);
+  EXPECT(std::fabs(effective_bandwidth(128, 4096, 100, 4, 1.0) - 0.2114048) < 1e-12);
+  auto u = uniform_fill(4, 7);
+  EXPECT(u.size() == 4 && u[0] >= -1.0 && u[0] < 1.0);
+  std::vector<ConfigResult> rows = {{parse_precision_config("ddddd"), 2.0, 2.0, 2.0, 0.0},
+                                    {parse_precision_config("dssdd"), 1.0, 1.0, 1.0, 1e-8},
+                                    {parse_precision_config("sssss"), 1.5, 1.5, 1.5, 1e-6}};
+  auto front = pareto_front(rows);
+  EXPECT(front.size() == 2);
+  EXPECT(optimal_config(rows, 1e-7).render() == "dssdd");
+  EXPECT(optimal_config(rows, 1e-9).render() == "ddddd");
+  SweepReport rep = make_report(ProblemDims(3, 2, 4), MatvecKind::Forward, 1, 1e-7, rows);
+  auto back = parse_sweep_csv(to_csv(rep));
+  EXPECT(back.size() == 3 && back[1].config.render() == "dssdd" && back[2].rel_error == 1e-6);
+  BlockVector v = BlockVector::time_double(2, 3, {1, 2, 3, 4, 5, 6});
+  auto t = reorder(v, Layout::TOSI);
+  EXPECT(t.f64[1] == 4 && reorder(t, Layout::SOTI).f64 == v.f64);
+}
+
+// direct block-Toeplitz products (dense_ref.hpp semantics), for the check only
+static std::vector<double> dense(const BlockColumn& c, const std::vector<double>& x, bool fwd) {
+  const auto& d = c.dims;
+  std::vector<double> y((fwd ? d.n_d : d.n_m) * d.n_t, 0.0);
+  for (std::size_t i = 0; i < d.n_t; ++i)
+    for (std::size_t j = 0; j <= i; ++j)
+      for (std::size_t col = 0; col < d.n_m; ++col)
+        for (std::size_t r = 0; r < d.n_d; ++r) {
+          if (fwd)
+            y[r * d.n_t + i] += c.at(i - j, r, col) * x[col * d.n_t + j];
+          else
+            y[col * d.n_t + j] += c.at(i - j, r, col) * x[r * d.n_t + i];
+        }
+  return y;
+}
+
+static void gpu_checks() {
+  const ProblemDims dims(16, 4, 32);
+  BlockColumn col(dims, uniform_fill(dims.n_t * dims.n_d * dims.n_m, seed_stream(20250814, 0)));
+  const auto m = uniform_fill(dims.n_m * dims.n_t, seed_stream(20250814, 1));
+  const auto d = uniform_fill(dims.n_d * dims.n_t, seed_stream(20250814, 2));
+  SpectralOperator op = setup_operator(col);
+  EXPECT(op.bins_double.size() == dims.n_bins() * dims.n_d * dims.n_m);
+  reset_cast_counter();
+  auto F = forward_matvec(op, BlockVector::time_double(dims.n_m, dims.n_t, m), PrecisionConfig::all_double());
+  auto A = adjoint_matvec(op, BlockVector::time_double(dims.n_d, dims.n_t, d), parse_precision_config("ddddd"));
+  EXPECT(casts_performed() == 0);
+  const double ef = relative_error(F.output.f64, dense(col, m, true));
+  const double ea = relative_error(A.output.f64, dense(col, d, false));
+  std::printf("  forward vs dense %.3e, adjoint vs dense %.3e\n", ef, ea);
+  EXPECT(ef <= 1e-12 && ea <= 1e-12);
+  double lhs = 0, rhs = 0;
+  for (std::size_t i = 0; i < d.size(); ++i) lhs += F.output.f64[i] * d[i];
+  for (std::size_t i = 0; i < m.size(); ++i) rhs += m[i] * A.output.f64[i];
+  EXPECT(std::fabs(lhs - rhs) <= 1e-11 * std::fabs(lhs));
+  // delta column: d_i = B m_i
+  BlockColumn delta = BlockColumn::zeros(dims);
+  for (std::size_t k = 0; k < dims.n_d * dims.n_m; ++k) delta.data[k] = col.data[k];
+  auto Fd = forward_matvec(setup_operator(delta), BlockVector::time_double(dims.n_m, dims.n_t, m),
+                           PrecisionConfig::all_double());
+  EXPECT(relative_error(Fd.output.f64, dense(delta, m, true)) <= 1e-12);
+  // partitions: p=1 bitwise, p=2,4 within 1e-12
+  for (std::size_t p : {1u, 2u, 4u}) {
+    auto pop = setup_partitioned(col, Grid1xP::split(p, dims.n_m));
+    auto pf = forward_matvec_partitioned(pop, BlockVector::time_double(dims.n_m, dims.n_t, m), PrecisionConfig{});
+    auto pa = adjoint_matvec_partitioned(pop, BlockVector::time_double(dims.n_d, dims.n_t, d), PrecisionConfig{});
+    if (p == 1) EXPECT(pf.output.f64 == F.output.f64 && pa.output.f64 == A.output.f64);
+    EXPECT(relative_error(pf.output.f64, F.output.f64) <= 1e-12);
+    EXPECT(relative_error(pa.output.f64, A.output.f64) <= 1e-12);
+  }
+  // FFT facade round trip
+  FftPlan fwd(16, 3, Precision::Double, FftDirection::Forward), inv(16, 3, Precision::Double, FftDirection::Inverse);
+  auto x = uniform_fill(48, 3);
+  auto X = forward_real_batched(fwd, x);
+  auto xr = inverse_real_batched(inv, X);
+  EXPECT(relative_error(xr, x) <= 1e-12);
+  // GEMV facade: ConjTrans of [[i,0],[0,i]] times (1,1) = (-i,-i)
+  std::vector<std::complex<double>> Am = {{0, 1}, {0, 0}, {0, 0}, {0, 1}}, xv = {{1, 0}, {1, 0}}, yv(2);
+  gemv_batched_auto(GemvMode::ConjTrans, MatrixBatch<std::complex<double>>::tight(Am, 2, 2, 1),
+                    VectorBatch<const std::complex<double>>::tight(xv, 2, 1),
+                    VectorBatch<std::complex<double>>::tight(yv, 2, 1));
+  EXPECT(yv[0] == std::complex<double>(0, -1) && yv[1] == std::complex<double>(0, -1));
+  // sweep: 32 rows, baseline error 0, optimal within tolerance
+  auto rows = sweep_configs(op, m, MatvecKind::Forward, 2, 1);
+  EXPECT(rows.size() == 32 && rows[0].rel_error == 0.0);
+  auto rep = make_report(dims, MatvecKind::Forward, 2, 1e-5, rows);
+  EXPECT(std::find_if(rows.begin(), rows.end(), [&](auto& r) { return r.config == rep.chosen; })->rel_error <= 1e-5);
+}
+
+int main(int argc, char** argv) {
+  host_checks();
+  if (argc > 1 && std::strcmp(argv[1], "--gpu") == 0) gpu_checks();
+  std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+  return failures ? 1 : 0;
+}
