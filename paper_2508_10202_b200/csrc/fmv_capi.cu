@@ -450,9 +450,9 @@ int env_int(const char* name, int dflt) {
   return v && *v ? atoi(v) : dflt;
 }
 
-template <int MODE, class E, class O, int RPT>
+template <int MODE, class E, class O, int RPT, int V, int LPC>
 void sbgemv_launch_t(fmv_ctx* ctx, GemvPlan& gp) {
-  auto kern = k_sbgemv<MODE, E, O, RPT>;
+  auto kern = k_sbgemv<MODE, E, O, RPT, V, LPC>;
   prep_smem((const void*)kern, gp.smem);
   static std::mutex mu;
   static std::map<std::tuple<int, int, size_t>, int> occ_cache;
@@ -491,12 +491,13 @@ void sbgemv_simple_t(fmv_ctx* ctx, GemvPlan& gp) {
 
 constexpr int kConsumers = 256;  // consumer threads per CTA (+1 producer warp); __launch_bounds__(288, 2)
 
-// Fills the staged-kernel plan; returns false when the staged kernel's
-// limits (m <= 1024 rows for NoTrans, stage fits) are exceeded.
-bool plan_staged(GemvPlan& gp, int mode, size_t es, size_t accsz) {
+// Fills the staged-kernel plan for V-element (16-byte) row vectors; returns
+// false when the staged kernel's limits are exceeded (NoTrans: m > 4*256*V
+// rows; a stage that does not fit shared memory).
+bool plan_staged(GemvPlan& gp, int mode, size_t es, size_t accsz, int V) {
   GemvParams& p = gp.p;
   const long col_bytes = p.lda * (long)es;
-  const int a_target = env_int("FMV_SBGEMV_STAGE_BYTES", 24 * 1024);
+  const int a_target = env_int("FMV_SBGEMV_STAGE_BYTES", 32 * 1024);
   int Jc = (int)std::max<long>(1, a_target / std::max<long>(col_bytes, 1));
   const long max_a = ((long)(Jc - 1) * p.lda + p.m) * (long)es;
   if (max_a > 96 * 1024) return false;
@@ -505,20 +506,21 @@ bool plan_staged(GemvPlan& gp, int mode, size_t es, size_t accsz) {
   p.a_slot = up128(max_a + 32);
   const long max_x = (mode == GM_N ? (long)Jc : (long)p.m) * (long)es;
   p.x_slot = up128(max_x + 32);
-  p.nstage = std::max(2, std::min(16, env_int("FMV_SBGEMV_STAGES", 4)));
+  p.nstage = std::max(2, std::min(16, env_int("FMV_SBGEMV_STAGES", 3)));
   size_t red = 0;
+  const int MV = (p.m + V - 1) / V;
   if (mode == GM_N) {
     int rpt = 1;
-    while ((p.m + rpt - 1) / rpt > kConsumers) rpt *= 2;
+    while ((MV + rpt - 1) / rpt > kConsumers) rpt *= 2;
     if (rpt > 4) return false;
-    p.RT = (p.m + rpt - 1) / rpt;
+    p.RT = (MV + rpt - 1) / rpt;
     p.G = std::max(1, kConsumers / p.RT);
     const int ncons = (p.RT * p.G + 31) / 32 * 32;
     gp.block = ncons + 32;
     gp.rpt = rpt;
     red = (size_t)p.G * p.m * accsz;
   } else {
-    p.LPC = p.m > 16 ? 32 : p.m > 8 ? 16 : p.m > 4 ? 8 : 4;
+    p.LPC = MV >= 8 ? 8 : 4;
     gp.block = kConsumers + 32;
   }
   gp.smem = 512 + (size_t)p.nstage * (p.a_slot + p.x_slot) + (red + 127) / 128 * 128;
@@ -526,21 +528,39 @@ bool plan_staged(GemvPlan& gp, int mode, size_t es, size_t accsz) {
   return true;
 }
 
+template <int MODE, class E, class O, int V>
+void sbgemv_staged_v(fmv_ctx* ctx, GemvPlan& gp) {
+  if constexpr (MODE == GM_N) {
+    if (gp.rpt == 1) sbgemv_launch_t<MODE, E, O, 1, V, 0>(ctx, gp);
+    else if (gp.rpt == 2) sbgemv_launch_t<MODE, E, O, 2, V, 0>(ctx, gp);
+    else sbgemv_launch_t<MODE, E, O, 4, V, 0>(ctx, gp);
+  } else {
+    if (gp.p.LPC == 8) sbgemv_launch_t<MODE, E, O, 1, V, 8>(ctx, gp);
+    else sbgemv_launch_t<MODE, E, O, 1, V, 4>(ctx, gp);
+  }
+}
+
 template <int MODE, class E, class O>
 void sbgemv_run_t(fmv_ctx* ctx, GemvPlan& gp, bool force_simple, int* used) {
-  const bool staged = !force_simple && plan_staged(gp, MODE, sizeof(E), sizeof(typename ET<E>::A));
+  constexpr int VMAX = (int)(16 / sizeof(E));
+  // 16-byte row vectors need 16-byte aligned columns (and x for (Conj)Trans)
+  const auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  bool vec = VMAX > 1 && gp.p.lda % VMAX == 0 && gp.p.sa % VMAX == 0 && al16(gp.p.A);
+  if (MODE != GM_N) vec = vec && gp.p.sx % VMAX == 0 && al16(gp.p.x);
+  const int V = vec ? VMAX : 1;
+  const bool staged = !force_simple && plan_staged(gp, MODE, sizeof(E), sizeof(typename ET<E>::A), V);
   if (used) *used = staged ? 0 : 1;
   if (!staged) {
     sbgemv_simple_t<MODE, E, O>(ctx, gp);
     return;
   }
-  if constexpr (MODE == GM_N) {
-    if (gp.rpt == 1) sbgemv_launch_t<MODE, E, O, 1>(ctx, gp);
-    else if (gp.rpt == 2) sbgemv_launch_t<MODE, E, O, 2>(ctx, gp);
-    else sbgemv_launch_t<MODE, E, O, 4>(ctx, gp);
-  } else {
-    sbgemv_launch_t<MODE, E, O, 1>(ctx, gp);
+  if constexpr (VMAX > 1) {
+    if (vec) {
+      sbgemv_staged_v<MODE, E, O, VMAX>(ctx, gp);
+      return;
+    }
   }
+  sbgemv_staged_v<MODE, E, O, 1>(ctx, gp);
 }
 
 template <class E, class O>
@@ -584,26 +604,29 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
   long lda = 0;
   const void* bins = op_bins(ctx, op, p[2], &lda);
   const size_t e2 = esize(p[2]), e3 = esize(p[3]);
-  ctx->x.ensure((size_t)nb * n_in * e2 + 256);
+  // TOSI stride of the spectrum padded to 4 elements so every bin's x_k starts
+  // 16-byte aligned (vectorized SBGEMV-C loads).
+  const long sx = (n_in + 3) / 4 * 4;
+  ctx->x.ensure((size_t)nb * sx * e2 + 256);
   ctx->y.ensure((size_t)nb * n_out * e3 + 256);
   // Phases 1-2 (+ reorder to TOSI, cast to cfg[2]).
   if (payload_prec < 0)
     r2c_dispatch<double>(ctx, p[0], p[1], p[2], static_cast<const double*>(in), nt, 1, n_in, (int)nt, (int)nt,
-                         ctx->x.p, n_in, 1);
+                         ctx->x.p, sx, 1);
   else if (payload_prec == PD)
     r2c_dispatch<double>(ctx, PD, p[1], p[2], static_cast<const double*>(in), nt, 1, n_in, (int)nt, (int)nt,
-                         ctx->x.p, n_in, 1);
+                         ctx->x.p, sx, 1);
   else if (payload_prec == PS)
     r2c_dispatch<float>(ctx, PS, p[1], p[2], static_cast<const float*>(in), nt, 1, n_in, (int)nt, (int)nt, ctx->x.p,
-                        n_in, 1);
+                        sx, 1);
   else
     r2c_dispatch<__half>(ctx, PH, p[1], p[2], static_cast<const __half*>(in), nt, 1, n_in, (int)nt, (int)nt,
-                         ctx->x.p, n_in, 1);
+                         ctx->x.p, sx, 1);
   if (ev_r2c) CK(cudaEventRecord(ev_r2c, ctx->stream));
   // Phase 3 SBGEMV in cfg[2], output cast to cfg[3], TOSI.
   const long m = (long)op->nd, n = (long)op->nm;
-  GemvPlan gp = fwd ? make_gemv(bins, m, n, nb, lda, n * lda, ctx->x.p, n, ctx->y.p, m)
-                    : make_gemv(bins, m, n, nb, lda, n * lda, ctx->x.p, m, ctx->y.p, n);
+  GemvPlan gp = fwd ? make_gemv(bins, m, n, nb, lda, n * lda, ctx->x.p, sx, ctx->y.p, m)
+                    : make_gemv(bins, m, n, nb, lda, n * lda, ctx->x.p, sx, ctx->y.p, n);
   const int mode = fwd ? GM_N : GM_C;
   if (p[2] == PD) {
     if (p[3] == PD) sbgemv_mode<double2, double2>(ctx, mode, gp, false, nullptr);

@@ -58,6 +58,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Consumer wait: same parity protocol, with a suspend-time hint so a waiting
+// warp sleeps in the barrier unit instead of spinning on the issue port.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n"
+      "DONE:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x100000)
+      : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -131,17 +144,36 @@ struct ET<float2> {
     return make_float2(__shfl_xor_sync(0xffffffffu, a.x, o), __shfl_xor_sync(0xffffffffu, a.y, o));
   }
 };
-// fp16 storage, fp32 accumulation (the 'h' extension).
+// fp16 storage, fp32 accumulation (the 'h' extension). Blackwell's
+// mixed-precision FMA (fma.rn.f32.f16 -> SASS FHFMA, half-register selectors
+// and negation folded) does f32 += f16*f16 in one instruction; the f16
+// product is exact in f32, so this equals convert-then-FFMA bit for bit.
+__device__ __forceinline__ float fhfma(__half a, __half b, float c) {
+  float d;
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d) : "h"(__half_as_ushort(a)), "h"(__half_as_ushort(b)), "f"(c));
+  return d;
+}
+__device__ __forceinline__ __half hlo(__half2 v) { return __low2half(v); }
+__device__ __forceinline__ __half hhi(__half2 v) { return __high2half(v); }
+__device__ __forceinline__ __half hneg(__half v) { return __hneg(v); }
 template <>
 struct ET<__half2> {
   using A = float2;
   static constexpr bool cplx = true;
   static __device__ __forceinline__ A zero() { return make_float2(0.f, 0.f); }
-  static __device__ __forceinline__ A mac(A c, __half2 a, __half2 x) {
-    return ET<float2>::mac(c, __half22float2(a), __half22float2(x));
+  static __device__ __forceinline__ A mac(A c, __half2 a, __half2 x) {  // c += a*x
+    c.x = fhfma(hlo(a), hlo(x), c.x);
+    c.x = fhfma(hneg(hhi(a)), hhi(x), c.x);
+    c.y = fhfma(hlo(a), hhi(x), c.y);
+    c.y = fhfma(hhi(a), hlo(x), c.y);
+    return c;
   }
-  static __device__ __forceinline__ A macc(A c, __half2 a, __half2 x) {
-    return ET<float2>::macc(c, __half22float2(a), __half22float2(x));
+  static __device__ __forceinline__ A macc(A c, __half2 a, __half2 x) {  // c += conj(a)*x
+    c.x = fhfma(hlo(a), hlo(x), c.x);
+    c.x = fhfma(hhi(a), hhi(x), c.x);
+    c.y = fhfma(hlo(a), hhi(x), c.y);
+    c.y = fhfma(hneg(hhi(a)), hlo(x), c.y);
+    return c;
   }
   static __device__ __forceinline__ A add(A a, A b) { return ET<float2>::add(a, b); }
   static __device__ __forceinline__ A shfl_xor(A a, int o) { return ET<float2>::shfl_xor(a, o); }
@@ -223,21 +255,61 @@ __device__ __forceinline__ long piece_of(long c, long T, int P) {
   return ((c + 1) * (long)P - 1) / T;
 }
 
-struct Seg {
-  long b, j, cnt;
+// Walks the flat column stream of one piece, one stage-sized segment at a
+// time, without per-stage 64-bit divisions: (b, j) = (batch entry, column),
+// cnt = columns in this segment (never crosses a batch entry), ring slot s
+// and its mbarrier phase parity advance incrementally.
+struct SegIter {
+  long b, j, c, c1, cnt;
+  int s;
+  uint32_t par;
+  __device__ __forceinline__ SegIter(long c0, long c1_, const GemvParams& p) : c(c0), c1(c1_), s(0), par(0) {
+    b = c0 / p.n;
+    j = c0 - b * p.n;
+    cnt = 0;
+  }
+  __device__ __forceinline__ bool more() const { return c < c1; }
+  __device__ __forceinline__ void load(const GemvParams& p) {
+    long k = p.Jc;
+    k = min(k, c1 - c);
+    k = min(k, p.n - j);
+    cnt = k;
+  }
+  // true when this segment closed batch entry b (or the piece)
+  __device__ __forceinline__ bool ends_bin(const GemvParams& p) const { return j + cnt == p.n || c + cnt == c1; }
+  __device__ __forceinline__ void advance(const GemvParams& p) {
+    c += cnt;
+    j += cnt;
+    if (j == p.n) {
+      j = 0;
+      ++b;
+    }
+    if (++s == p.nstage) {
+      s = 0;
+      par ^= 1u;
+    }
+  }
 };
-__device__ __forceinline__ Seg next_seg(long c, long c1, const GemvParams& p) {
-  Seg s;
-  s.b = c / p.n;
-  s.j = c - s.b * p.n;
-  long cnt = p.Jc;
-  cnt = min(cnt, c1 - c);
-  cnt = min(cnt, p.n - s.j);
-  s.cnt = cnt;
-  return s;
+
+// V elements of E packed in one 16-byte shared-memory load.
+template <class E, int V>
+struct alignas(V == 1 ? alignof(E) : 16) VecT {
+  E e[V];
+};
+template <class E, int V>
+__device__ __forceinline__ VecT<E, V> ldv(const E* p) {
+  if constexpr (V == 1) {
+    return VecT<E, 1>{{*p}};
+  } else {
+    static_assert(sizeof(E) * V == 16, "vector must be 16 bytes");
+    const int4 raw = *reinterpret_cast<const int4*>(p);
+    VecT<E, V> r;
+    memcpy(&r, &raw, 16);
+    return r;
+  }
 }
 
-template <int MODE, class E, class O, int RPT>
+template <int MODE, class E, class O, int RPT, int V, int LPC>
 __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
   using Tr = ET<E>;
   using Acc = typename Tr::A;
@@ -268,12 +340,10 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
     if (threadIdx.x != ncons) return;
     const uint64_t pol_a = policy_evict_first();
     const uint64_t pol_x = policy_evict_last();
-    long it = 0;
-    for (long c = c0; c < c1; ++it) {
-      const Seg sg = next_seg(c, c1, p);
-      const int s = (int)(it % p.nstage);
-      const uint32_t par = (uint32_t)((it / p.nstage) & 1);
-      mbar_wait(&empty[s], par ^ 1u);
+    for (SegIter sg(c0, c1, p); sg.more(); sg.advance(p)) {
+      sg.load(p);
+      const int s = sg.s;
+      mbar_wait(&empty[s], sg.par ^ 1u);
       const unsigned char* a0 = p.A + (sg.b * p.sa + sg.j * p.lda) * es;
       const unsigned char* a_lo = reinterpret_cast<const unsigned char*>(reinterpret_cast<uintptr_t>(a0) & ~uintptr_t(15));
       const uintptr_t a_end = reinterpret_cast<uintptr_t>(a0) + (uintptr_t)(((sg.cnt - 1) * p.lda + p.m) * es);
@@ -287,7 +357,6 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
       mbar_expect_tx(&full[s], a_bytes + x_bytes);
       bulk_g2s(dst, a_lo, a_bytes, &full[s], pol_a);
       bulk_g2s(dst + p.a_slot, x_lo, x_bytes, &full[s], pol_x);
-      c += sg.cnt;
     }
     return;
   }
@@ -295,24 +364,26 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
   // ---------------------------------------------------- consumers ----
   const int t = threadIdx.x;
   const int lane = t & 31;
+  const int MV = (p.m + V - 1) / V;  // 16-byte row vectors per column (V elements each)
   if constexpr (MODE == GM_N) {
+    // thread (r, g): row vectors r, r+RT, ... (RPT of them), columns g, g+G, ...
     const int r = t % p.RT;
     const int g = t / p.RT;
     const bool active = g < p.G;
-    Acc acc[RPT];
+    Acc acc[RPT][V];
 #pragma unroll
-    for (int q = 0; q < RPT; ++q) acc[q] = Tr::zero();
-    long it = 0;
-    for (long c = c0; c < c1; ++it) {
-      const Seg sg = next_seg(c, c1, p);
-      const int s = (int)(it % p.nstage);
-      const uint32_t par = (uint32_t)((it / p.nstage) & 1);
+    for (int q = 0; q < RPT; ++q)
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[q][v] = Tr::zero();
+    for (SegIter sg(c0, c1, p); sg.more(); sg.advance(p)) {
+      sg.load(p);
+      const int s = sg.s;
       const unsigned char* a0 = p.A + (sg.b * p.sa + sg.j * p.lda) * es;
       const unsigned char* x0 = p.x + (sg.b * p.sx + sg.j) * es;
       const unsigned char* base = stages + (long)s * slot;
       const E* As = reinterpret_cast<const E*>(base + (reinterpret_cast<uintptr_t>(a0) & 15));
       const E* Xs = reinterpret_cast<const E*>(base + p.a_slot + (reinterpret_cast<uintptr_t>(x0) & 15));
-      mbar_wait(&full[s], par);
+      mbar_wait_sleep(&full[s], sg.par);
       if (active) {
         const int cnt = (int)sg.cnt;
         for (int jj = g; jj < cnt; jj += p.G) {
@@ -320,25 +391,30 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
           const E* col = As + (long)jj * p.lda;
 #pragma unroll
           for (int q = 0; q < RPT; ++q) {
-            const int row = r + q * p.RT;
-            if (row < p.m) acc[q] = Tr::mac(acc[q], col[row], xv);
+            const int vi = r + q * p.RT;
+            if (vi < MV) {
+              const VecT<E, V> a = ldv<E, V>(col + vi * V);
+#pragma unroll
+              for (int v = 0; v < V; ++v) acc[q][v] = Tr::mac(acc[q][v], a.e[v], xv);
+            }
           }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      c += sg.cnt;
-      if (sg.j + sg.cnt == p.n || c == c1) {
+      if (sg.ends_bin(p)) {
         // ---- flush bin sg.b: intra-CTA reduction over column groups ----
         if (active) {
 #pragma unroll
           for (int q = 0; q < RPT; ++q) {
-            const int row = r + q * p.RT;
-            if (row < p.m) red[(long)g * p.m + row] = acc[q];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              const int row = (r + q * p.RT) * V + v;
+              if (row < p.m) red[(long)g * p.m + row] = acc[q][v];
+              acc[q][v] = Tr::zero();
+            }
           }
         }
-#pragma unroll
-        for (int q = 0; q < RPT; ++q) acc[q] = Tr::zero();
         bar_consumers(ncons);
         for (int i = t; i < p.m; i += ncons) {
           Acc v = red[i];
@@ -378,43 +454,58 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
       }
     }
   } else {
-    // (Conj)Trans: LPC lanes per column, CPW columns per warp-iteration.
+    // (Conj)Trans: every consumer warp visits every stage (so every waiter
+    // sees consecutive mbarrier phases); the stage's columns are dealt out
+    // CPW at a time across the W warps, LPC lanes per column, 16-byte vector
+    // loads, two accumulator chains and a fixed xor-shuffle tree per column.
+    constexpr int CPW = 32 / LPC;
     const int W = ncons / 32;
     const int w = t >> 5;
-    const int LPC = p.LPC;
-    const int CPW = 32 / LPC;
     const int sub = lane / LPC;
     const int li = lane - sub * LPC;
-    long it = 0;
-    for (long c = c0; c < c1; ++it) {
-      const Seg sg = next_seg(c, c1, p);
-      const int s = (int)(it % p.nstage);
-      const uint32_t par = (uint32_t)((it / p.nstage) & 1);
+    const bool ragged = (p.m % V) != 0;
+    for (SegIter sg(c0, c1, p); sg.more(); sg.advance(p)) {
+      sg.load(p);
+      const int s = sg.s;
       const unsigned char* a0 = p.A + (sg.b * p.sa + sg.j * p.lda) * es;
       const unsigned char* x0 = p.x + sg.b * p.sx * es;
       const unsigned char* base = stages + (long)s * slot;
       const E* As = reinterpret_cast<const E*>(base + (reinterpret_cast<uintptr_t>(a0) & 15));
       const E* Xs = reinterpret_cast<const E*>(base + p.a_slot + (reinterpret_cast<uintptr_t>(x0) & 15));
       O* yb = reinterpret_cast<O*>(p.y) + sg.b * p.sy + sg.j;
-      mbar_wait(&full[s], par);
+      mbar_wait_sleep(&full[s], sg.par);
       const int cnt = (int)sg.cnt;
       for (int jb = w * CPW; jb < cnt; jb += W * CPW) {
         const int jj = jb + sub;
         const bool valid = jj < cnt;
-        Acc a = Tr::zero();
+        Acc a0c = Tr::zero(), a1c = Tr::zero();
         if (valid) {
           const E* col = As + (long)jj * p.lda;
-          for (int i = li; i < p.m; i += LPC) {
-            if constexpr (MODE == GM_C) a = Tr::macc(a, col[i], Xs[i]);
-            else a = Tr::mac(a, col[i], Xs[i]);
+          auto body = [&](Acc& acc, int vi) {
+            const VecT<E, V> a = ldv<E, V>(col + vi * V);
+            const VecT<E, V> x = ldv<E, V>(Xs + vi * V);
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              if (V == 1 || !ragged || vi * V + v < p.m) {
+                if constexpr (MODE == GM_C) acc = Tr::macc(acc, a.e[v], x.e[v]);
+                else acc = Tr::mac(acc, a.e[v], x.e[v]);
+              }
+            }
+          };
+          int vi = li;
+          for (; vi + LPC < MV; vi += 2 * LPC) {
+            body(a0c, vi);
+            body(a1c, vi + LPC);
           }
+          if (vi < MV) body(a0c, vi);
         }
+        Acc a = Tr::add(a0c, a1c);
+#pragma unroll
         for (int o = LPC >> 1; o > 0; o >>= 1) a = Tr::add(a, Tr::shfl_xor(a, o));
         if (valid && li == 0) yb[jj] = out_cast<O>(a);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      c += sg.cnt;
     }
   }
 }
