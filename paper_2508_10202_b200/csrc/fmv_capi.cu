@@ -123,10 +123,13 @@ size_t esize(int prec) { return prec == PD ? 16 : prec == PS ? 8 : 4; }
 // ======================================================================
 // FFT geometry + twiddle tables (per device, per L, per precision)
 // ======================================================================
-FftGeom make_geom(int Nt) {
+FftGeom make_geom(int Nt, int nout) {
   FftGeom g{};
   g.N = Nt;
   g.L = 2 * Nt;
+  g.n_div = FastDiv((uint32_t)Nt);
+  g.nb_div = FastDiv((uint32_t)Nt + 1);
+  g.nout_div = FastDiv((uint32_t)nout);
   int n = Nt;
   while (n > 1) {
     int r;
@@ -142,6 +145,13 @@ FftGeom make_geom(int Nt) {
     if (g.nst >= kMaxStages) fail(FMV_EUNSUPPORTED, "FFT: too many stages");
     g.radix[g.nst++] = r;
     n /= r;
+  }
+  int Ns = 1;
+  for (int st = 0; st < g.nst; ++st) {
+    g.nr_div[st] = FastDiv((uint32_t)(Nt / g.radix[st]));
+    g.ns_div[st] = FastDiv((uint32_t)Ns);
+    g.span_div[st] = FastDiv((uint32_t)(Ns * g.radix[st]));
+    Ns *= g.radix[st];
   }
   return g;
 }
@@ -196,6 +206,13 @@ struct TwiddleCache {
 TwiddleCache& twiddles() {
   static TwiddleCache* c = new TwiddleCache;  // intentionally leaked: outlives static destructors
   return *c;
+}
+
+// Tunables (env overridable for on-GPU sweeps): SBGEMV stage bytes / ring
+// depth / CTAs per SM, FFT shared-memory budget.
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
 }
 
 // Raise a kernel's dynamic shared-memory cap once per (function, size).
@@ -361,12 +378,15 @@ void launch(fmv_ctx* ctx, int cls, Fn&& fn) {
   }
 }
 
-int fft_series_per_cta(int N, size_t celem) {
+// log2 of the series per CTA (a power of two, <= 16) for a 64 KB smem budget.
+int fft_lg_series_per_cta(int N, size_t celem) {
   const size_t per = 2 * (size_t)(N + 1) * celem;
   if (per > 200 * 1024)
     fail(FMV_EUNSUPPORTED, "FFT: n_t = " + std::to_string(N) + " exceeds the shared-memory FFT capacity");
-  const size_t budget = 64 * 1024;
-  return (int)std::max<size_t>(1, std::min<size_t>(16, budget / per));
+  const size_t budget = (size_t)env_int("FMV_FFT_SMEM_BUDGET", 64 * 1024);
+  int lg = 0;
+  while (lg < 4 && per * ((size_t)2 << lg) <= budget) ++lg;
+  return lg;
 }
 
 template <int C0, int C1, int C2, class Tin>
@@ -374,8 +394,9 @@ void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, in
            long out_ks, long out_ss) {
   using R = typename PT<C1>::real;
   using C = typename CT<R>::c;
-  const FftGeom g = make_geom(N);
-  const int S = fft_series_per_cta(g.N, sizeof(C));
+  const FftGeom g = make_geom(N, nvalid);
+  const int lgS = fft_lg_series_per_cta(g.N, sizeof(C));
+  const int S = 1 << lgS;
   const size_t smem = 2 * (size_t)S * (g.N + 1) * sizeof(C);
   auto kern = k_r2c<C0, C1, C2, Tin>;
   prep_smem((const void*)kern, smem);
@@ -383,7 +404,7 @@ void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, in
   const long grid = (nseries + S - 1) / S;
   launch(ctx, 0, [&] {
     kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(in, in_ss, in_ts, nseries, nvalid,
-                                                     static_cast<typename PT<C2>::cplx*>(out), out_ks, out_ss, g, tw, S);
+                                                     static_cast<typename PT<C2>::cplx*>(out), out_ks, out_ss, g, tw, lgS);
   });
 }
 
@@ -411,8 +432,9 @@ template <int C3, int C4, class Tout>
 void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, int N, int nout, Tout* out,
            long out_ss) {
   using C = typename PT<C3>::cplx;
-  const FftGeom g = make_geom(N);
-  const int S = fft_series_per_cta(g.N, sizeof(C));
+  const FftGeom g = make_geom(N, nout);
+  const int lgS = fft_lg_series_per_cta(g.N, sizeof(C));
+  const int S = 1 << lgS;
   const size_t smem = 2 * (size_t)S * (g.N + 1) * sizeof(C);
   auto kern = k_c2r<C3, C4, Tout>;
   prep_smem((const void*)kern, smem);
@@ -420,7 +442,7 @@ void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, i
   const long grid = (nseries + S - 1) / S;
   launch(ctx, 3, [&] {
     kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(static_cast<const C*>(in), in_ks, in_ss, nseries, nout, out,
-                                                     out_ss, g, tw, S);
+                                                     out_ss, g, tw, lgS);
   });
 }
 
@@ -444,11 +466,6 @@ struct GemvPlan {
   int rpt = 1;
 };
 
-// Tunables (env overridable for on-GPU sweeps): A-stage bytes and ring depth.
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
 
 template <int MODE, class E, class O, int RPT, int V, int LPC>
 void sbgemv_launch_t(fmv_ctx* ctx, GemvPlan& gp) {

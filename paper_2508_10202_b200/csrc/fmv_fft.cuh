@@ -25,11 +25,31 @@ namespace fmv {
 
 constexpr int kMaxStages = 24;
 
+// Division by a runtime-invariant divisor with one multiply-high
+// (Granlund-Montgomery round-up method; valid for n < 2^31).
+struct FastDiv {
+  uint32_t d = 1, m = 0, s = 0;
+  FastDiv() = default;
+  explicit FastDiv(uint32_t div) : d(div) {
+    if (div > 1) {
+      while ((1u << s) < div) ++s;
+      m = (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << s) - div)) / div + 1);
+    }
+  }
+  __device__ __forceinline__ int div(int n) const {
+    return d == 1 ? n : (int)((__umulhi((uint32_t)n, m) + (uint32_t)n) >> s);
+  }
+};
+
 struct FftGeom {
   int N;  // complex length = L/2 = Nt
   int L;  // real length 2*Nt
   int nst;
   int radix[kMaxStages];
+  FastDiv nr_div[kMaxStages];    // N / radix (work items per series)
+  FastDiv ns_div[kMaxStages];    // Ns (product of earlier radices)
+  FastDiv span_div[kMaxStages];  // Ns * radix
+  FastDiv n_div, nb_div, nout_div;  // N, N + 1, output samples per series
 };
 
 template <class R>
@@ -119,22 +139,23 @@ __device__ __forceinline__ C twiddle(const C* __restrict__ tw, int e) {
 
 template <class R, int D, int Rn>
 __device__ __forceinline__ void stage_fixed(const typename CT<R>::c* __restrict__ src, typename CT<R>::c* __restrict__ dst,
-                                            int N, int ss, int ns, int Ns, const typename CT<R>::c* __restrict__ tw,
-                                            int L) {
+                                            int ss, int ns, int Ns, const FastDiv& nrd, const FastDiv& nsd,
+                                            const typename CT<R>::c* __restrict__ tw, int N, int L) {
   using C = typename CT<R>::c;
   const int Nr = N / Rn;
   const int tstep = L / (Ns * Rn);
   for (int it = threadIdx.x; it < ns * Nr; it += blockDim.x) {
-    const int s = it / Nr;
+    const int s = nrd.div(it);
     const int j = it - s * Nr;
-    const int k = j % Ns;
+    const int k = j - nsd.div(j) * Ns;
     const C* in = src + s * ss;
     C v[Rn];
 #pragma unroll
     for (int q = 0; q < Rn; ++q) v[q] = in[j + q * Nr];
     if (Ns > 1) {
+      const int kt = k * tstep;
 #pragma unroll
-      for (int q = 1; q < Rn; ++q) v[q] = cmul(v[q], twiddle<D>(tw, q * k * tstep));
+      for (int q = 1; q < Rn; ++q) v[q] = cmul(v[q], twiddle<D>(tw, q * kt));
     }
     butterfly<R, D, Rn>(v);
     C* out = dst + s * ss + (j - k) * Rn + k;
@@ -146,18 +167,19 @@ __device__ __forceinline__ void stage_fixed(const typename CT<R>::c* __restrict_
 // Any radix r (used for primes other than 2,3,5): one thread per output.
 template <class R, int D>
 __device__ __forceinline__ void stage_generic(const typename CT<R>::c* __restrict__ src,
-                                              typename CT<R>::c* __restrict__ dst, int N, int ss, int ns, int r, int Ns,
-                                              const typename CT<R>::c* __restrict__ tw, int L) {
+                                              typename CT<R>::c* __restrict__ dst, int ss, int ns, int r, int Ns,
+                                              const FastDiv& nd, const FastDiv& nsd, const FastDiv& spand,
+                                              const typename CT<R>::c* __restrict__ tw, int N, int L) {
   using C = typename CT<R>::c;
   const int Nr = N / r;
   const int span = Ns * r;
   const int tstep = L / span;
   for (int it = threadIdx.x; it < ns * N; it += blockDim.x) {
-    const int s = it / N;
+    const int s = nd.div(it);
     const int o = it - s * N;
-    const int blk = o / span;
+    const int blk = spand.div(o);
     const int rem = o - blk * span;
-    const int q = rem / Ns;
+    const int q = nsd.div(rem);
     const int k = rem - q * Ns;
     const int j = blk * Ns + k;
     const int estep = k + q * Ns;
@@ -181,12 +203,14 @@ __device__ typename CT<R>::c* run_stages(typename CT<R>::c* a, typename CT<R>::c
   for (int st = 0; st < g.nst; ++st) {
     const int r = g.radix[st];
     switch (r) {
-      case 2: stage_fixed<R, D, 2>(a, b, g.N, ss, ns, Ns, tw, g.L); break;
-      case 3: stage_fixed<R, D, 3>(a, b, g.N, ss, ns, Ns, tw, g.L); break;
-      case 4: stage_fixed<R, D, 4>(a, b, g.N, ss, ns, Ns, tw, g.L); break;
-      case 5: stage_fixed<R, D, 5>(a, b, g.N, ss, ns, Ns, tw, g.L); break;
-      case 8: stage_fixed<R, D, 8>(a, b, g.N, ss, ns, Ns, tw, g.L); break;
-      default: stage_generic<R, D>(a, b, g.N, ss, ns, r, Ns, tw, g.L); break;
+      case 2: stage_fixed<R, D, 2>(a, b, ss, ns, Ns, g.nr_div[st], g.ns_div[st], tw, g.N, g.L); break;
+      case 3: stage_fixed<R, D, 3>(a, b, ss, ns, Ns, g.nr_div[st], g.ns_div[st], tw, g.N, g.L); break;
+      case 4: stage_fixed<R, D, 4>(a, b, ss, ns, Ns, g.nr_div[st], g.ns_div[st], tw, g.N, g.L); break;
+      case 5: stage_fixed<R, D, 5>(a, b, ss, ns, Ns, g.nr_div[st], g.ns_div[st], tw, g.N, g.L); break;
+      case 8: stage_fixed<R, D, 8>(a, b, ss, ns, Ns, g.nr_div[st], g.ns_div[st], tw, g.N, g.L); break;
+      default:
+        stage_generic<R, D>(a, b, ss, ns, r, Ns, g.n_div, g.ns_div[st], g.span_div[st], tw, g.N, g.L);
+        break;
     }
     __syncthreads();
     typename CT<R>::c* t = a;
@@ -202,16 +226,17 @@ __device__ typename CT<R>::c* run_stages(typename CT<R>::c* a, typename CT<R>::c
 //   X = r2c_L(v) in C1 arithmetic                                  (matvec.hpp:132-141)
 //   out[k, s] = rnd_C2(X[k])                                       (matvec.hpp:155-165)
 // Input element (s,t) at in[s*in_ss + t*in_ts]; output bin k of series s at
-// out[k*out_ks + s*out_ss]. One CTA per S consecutive series.
+// out[k*out_ks + s*out_ss]. One CTA per S (a power of two) consecutive series.
 template <int C0, int C1, int C2, class Tin>
 __global__ void __launch_bounds__(256) k_r2c(const Tin* __restrict__ in, long in_ss, long in_ts, long nseries, int nvalid,
                                              typename PT<C2>::cplx* __restrict__ out, long out_ks, long out_ss,
                                              FftGeom g, const typename CT<typename PT<C1>::real>::c* __restrict__ tw,
-                                             int S) {
+                                             int lgS) {
   using R = typename PT<C1>::real;
   using C = typename CT<R>::c;
   using OutC = typename PT<C2>::cplx;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int S = 1 << lgS;
   const int N = g.N;
   const int ss = N + 1;
   C* bufA = reinterpret_cast<C*>(smem_raw);
@@ -219,23 +244,70 @@ __global__ void __launch_bounds__(256) k_r2c(const Tin* __restrict__ in, long in
   const long s0 = (long)blockIdx.x * S;
   const int ns = (int)min((long)S, nseries - s0);
 
+  // Loads are batched U per thread (all issued before any shared store) so a
+  // CTA pays the DRAM latency about once, not once per loop trip.
+  constexpr int U = 4;
+  const int T = blockDim.x;
   if (in_ts == 1) {
-    for (int e = threadIdx.x; e < ns * N; e += blockDim.x) {
-      const int s = e / N, n = e - s * N;
-      const Tin* p = in + (s0 + s) * in_ss;
-      const int t0 = 2 * n, t1 = 2 * n + 1;
-      const R a = t0 < nvalid ? (R)rnd<C0>(to_d(p[t0])) : R(0);
-      const R b = t1 < nvalid ? (R)rnd<C0>(to_d(p[t1])) : R(0);
-      bufA[s * ss + n] = C{a, b};
+    bool vec = false;
+    if constexpr (sizeof(Tin) == 8) {
+      vec = (in_ss % 2 == 0) && (nvalid % 2 == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
+    }
+    const int total = ns * N;
+    for (int base = threadIdx.x; base < total; base += U * T) {
+      C v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = base + u * T;
+        v[u] = C{R(0), R(0)};
+        if (e < total) {
+          const int s = g.n_div.div(e), n = e - s * N;
+          const Tin* p = in + (s0 + s) * in_ss;
+          const int t0 = 2 * n;
+          if (vec) {
+            if (t0 < nvalid) {
+              const double2 pr = __ldg(reinterpret_cast<const double2*>(p) + n);
+              v[u] = C{(R)rnd<C0>(pr.x), (R)rnd<C0>(pr.y)};
+            }
+          } else {
+            const R a = t0 < nvalid ? (R)rnd<C0>(to_d(p[t0])) : R(0);
+            const R b = t0 + 1 < nvalid ? (R)rnd<C0>(to_d(p[t0 + 1])) : R(0);
+            v[u] = C{a, b};
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = base + u * T;
+        if (e < total) {
+          const int s = g.n_div.div(e), n = e - s * N;
+          bufA[s * ss + n] = v[u];
+        }
+      }
     }
   } else {
-    for (int e = threadIdx.x; e < ns * N; e += blockDim.x) {
-      const int n = e / ns, s = e - n * ns;
-      const Tin* p = in + (s0 + s) * in_ss;
-      const int t0 = 2 * n, t1 = 2 * n + 1;
-      const R a = t0 < nvalid ? (R)rnd<C0>(to_d(p[(long)t0 * in_ts])) : R(0);
-      const R b = t1 < nvalid ? (R)rnd<C0>(to_d(p[(long)t1 * in_ts])) : R(0);
-      bufA[s * ss + n] = C{a, b};
+    const int total = S * N;
+    for (int base = threadIdx.x; base < total; base += U * T) {
+      C v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = base + u * T;
+        const int n = e >> lgS, s = e & (S - 1);
+        v[u] = C{R(0), R(0)};
+        if (e < total && s < ns) {
+          const Tin* p = in + (s0 + s) * in_ss;
+          const int t0 = 2 * n, t1 = 2 * n + 1;
+          const R a = t0 < nvalid ? (R)rnd<C0>(to_d(p[(long)t0 * in_ts])) : R(0);
+          const R b = t1 < nvalid ? (R)rnd<C0>(to_d(p[(long)t1 * in_ts])) : R(0);
+          v[u] = C{a, b};
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = base + u * T;
+        const int n = e >> lgS, s = e & (S - 1);
+        if (e < total && s < ns) bufA[s * ss + n] = v[u];
+      }
     }
   }
   __syncthreads();
@@ -244,21 +316,24 @@ __global__ void __launch_bounds__(256) k_r2c(const Tin* __restrict__ in, long in
   // Real-signal post-pass: X[k] = E[k] + w^k * (-i) * D[k], k = 0..N.
   const R half = R(0.5);
   const int nbins = N + 1;
-  for (int e = threadIdx.x; e < ns * nbins; e += blockDim.x) {
-    int s, k;
-    if (out_ss == 1) {
-      k = e / ns;
-      s = e - k * ns;
-    } else {
-      s = e / nbins;
-      k = e - s * nbins;
-    }
+  auto post = [&](int s, int k) {
     const C A = Z[s * ss + (k == N ? 0 : k)];
     const C B = cconj(Z[s * ss + (k == 0 ? 0 : N - k)]);
     const C E = {(A.x + B.x) * half, (A.y + B.y) * half};
     const C Dm = {(A.x - B.x) * half, (A.y - B.y) * half};
     const C X = cadd(E, cmul(__ldg(tw + k), cmuli<-1>(Dm)));
     out[(long)k * out_ks + (s0 + s) * out_ss] = cfrom_d<OutC>(to_cd(X));
+  };
+  if (out_ss == 1) {  // bin-major (TOSI): consecutive threads -> consecutive series
+    for (int e = threadIdx.x; e < S * nbins; e += blockDim.x) {
+      const int k = e >> lgS, s = e & (S - 1);
+      if (s < ns) post(s, k);
+    }
+  } else {
+    for (int e = threadIdx.x; e < ns * nbins; e += blockDim.x) {
+      const int s = g.nb_div.div(e), k = e - s * nbins;
+      post(s, k);
+    }
   }
 }
 
@@ -269,10 +344,11 @@ __global__ void __launch_bounds__(256) k_r2c(const Tin* __restrict__ in, long in
 template <int C3, int C4, class Tout>
 __global__ void __launch_bounds__(256) k_c2r(const typename PT<C3>::cplx* __restrict__ in, long in_ks, long in_ss,
                                              long nseries, int nout, Tout* __restrict__ out, long out_ss, FftGeom g,
-                                             const typename PT<C3>::cplx* __restrict__ tw, int S) {
+                                             const typename PT<C3>::cplx* __restrict__ tw, int lgS) {
   using R = typename PT<C3>::real;
   using C = typename CT<R>::c;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int S = 1 << lgS;
   const int N = g.N;
   const int ss = N + 1;
   C* bufA = reinterpret_cast<C*>(smem_raw);
@@ -281,24 +357,48 @@ __global__ void __launch_bounds__(256) k_c2r(const typename PT<C3>::cplx* __rest
   const int ns = (int)min((long)S, nseries - s0);
   const R inv_len = R(1) / (R)g.L;
   const int nbins = N + 1;
-  for (int e = threadIdx.x; e < ns * nbins; e += blockDim.x) {
-    int s, k;
-    if (in_ss == 1) {
-      k = e / ns;
-      s = e - k * ns;
-    } else {
-      s = e / nbins;
-      k = e - s * nbins;
-    }
-    C X = in[(long)k * in_ks + (s0 + s) * in_ss];
+  auto fix = [&](C X, int k) {
     X.x = X.x * inv_len;
     X.y = (k == 0 || k == N) ? R(0) : X.y * inv_len;
-    bufA[s * ss + k] = X;
+    return X;
+  };
+  constexpr int U = 4;
+  const int T = blockDim.x;
+  const bool tosi = in_ss == 1;
+  const int total = tosi ? S * nbins : ns * nbins;
+  for (int base = threadIdx.x; base < total; base += U * T) {
+    C v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = base + u * T;
+      int s, k;
+      if (tosi) {
+        k = e >> lgS;
+        s = e & (S - 1);
+      } else {
+        s = g.nb_div.div(e);
+        k = e - s * nbins;
+      }
+      if (e < total && s < ns) v[u] = in[(long)k * in_ks + (s0 + s) * in_ss];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = base + u * T;
+      int s, k;
+      if (tosi) {
+        k = e >> lgS;
+        s = e & (S - 1);
+      } else {
+        s = g.nb_div.div(e);
+        k = e - s * nbins;
+      }
+      if (e < total && s < ns) bufA[s * ss + k] = fix(v[u], k);
+    }
   }
   __syncthreads();
   // Z[k] = (X[k] + conj X[N-k]) + i * w^-k * (X[k] - conj X[N-k])
   for (int e = threadIdx.x; e < ns * N; e += blockDim.x) {
-    const int s = e / N, k = e - s * N;
+    const int s = g.n_div.div(e), k = e - s * N;
     const C A = bufA[s * ss + k];
     const C B = cconj(bufA[s * ss + N - k]);
     const C w = __ldg(tw + k);
@@ -308,7 +408,7 @@ __global__ void __launch_bounds__(256) k_c2r(const typename PT<C3>::cplx* __rest
   __syncthreads();
   const C* z = run_stages<R, 1>(bufB, bufA, ss, ns, g, tw);
   for (int e = threadIdx.x; e < ns * nout; e += blockDim.x) {
-    const int s = e / nout, t = e - s * nout;
+    const int s = g.nout_div.div(e), t = e - s * nout;
     const C v = z[s * ss + (t >> 1)];
     out[(s0 + s) * out_ss + t] = (Tout)rnd<C4>((double)((t & 1) ? v.y : v.x));
   }
