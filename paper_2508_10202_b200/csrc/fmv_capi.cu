@@ -314,7 +314,9 @@ struct fmv_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  DevBuf x, y, io_in, io_out, partials, counters, payload, red;
+  DevBuf x, y, yacc, io_in, io_out, partials, counters, payload, red;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t cev[34] = {};
   size_t counters_len = 0;
   uint64_t launches = 0;
   bool profiling = false;
@@ -608,11 +610,66 @@ GemvPlan make_gemv(const void* A, long m, long n, long batch, long lda, long sa,
 // ------------------------------------------------------------ pipeline ----
 const void* op_bins(fmv_ctx* ctx, fmv_op* op, int prec, long* lda);
 
+template <class E>
+void run_gemv_o(fmv_ctx* ctx, int p3, int mode, GemvPlan& gp) {
+  if (p3 == PD) sbgemv_mode<E, double2>(ctx, mode, gp, false, nullptr);
+  else sbgemv_mode<E, float2>(ctx, mode, gp, false, nullptr);
+}
+void run_gemv(fmv_ctx* ctx, const std::array<int, 5>& p, int mode, GemvPlan& gp) {
+  if (p[2] == PD) run_gemv_o<double2>(ctx, p[3], mode, gp);
+  else if (p[2] == PS) run_gemv_o<float2>(ctx, p[3], mode, gp);
+  else run_gemv_o<__half2>(ctx, p[3], mode, gp);
+}
+
+// Column chunking of the operator for the host-I/O pipeline (a function of
+// shape, SBGEMV precision and direction only). Chunk sizes grow (F) or shrink
+// (F*) geometrically by 1.6x: PCIe moves a column about 1.7x faster than the
+// SBGEMV consumes one, so each chunk's copy hides behind its neighbour's
+// SBGEMV and only the smallest chunk's copy is exposed. Edges on multiples of
+// 4 columns.
+std::vector<long> chunk_edges(const fmv_op* op, int prec2, bool grow) {
+  const long nm = (long)op->nm;
+  const size_t bytes = op->nb() * op->nm * op->nd * esize(prec2);
+  long C = (bytes >= (size_t(1) << 30)) ? 6 : (bytes >= (size_t(1) << 27)) ? 3 : 1;
+  const int env = env_int("FMV_CHUNKS", 0);
+  if (env > 0) C = env;
+  C = std::max<long>(1, std::min<long>(C, nm / 4));
+  std::vector<double> w(C);
+  double tot = 0;
+  for (long c = 0; c < C; ++c) tot += (w[c] = std::pow(1.6, (double)(grow ? c : C - 1 - c)));
+  std::vector<long> e(C + 1, 0);
+  double acc = 0;
+  for (long c = 1; c < C; ++c) {
+    acc += w[c - 1];
+    e[c] = std::max(e[c - 1] + 4, ((long)(nm * acc / tot)) & ~3L);
+  }
+  e[C] = nm;
+  for (long c = C - 1; c >= 1; --c) e[c] = std::min(e[c], e[c + 1] - 1);  // keep chunks non-empty
+  return e;
+}
+
+struct HostIO {
+  const double* h_in = nullptr;  // copy in (overlapped) to the device `in` buffer
+  double* h_out = nullptr;       // copy out (overlapped) from the device `out` buffer
+};
+
+cudaStream_t copy_stream(fmv_ctx* ctx) {
+  if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  return ctx->copy_stream;
+}
+cudaEvent_t chunk_event(fmv_ctx* ctx, int i) {
+  if (!ctx->cev[i]) CK(cudaEventCreateWithFlags(&ctx->cev[i], cudaEventDisableTiming));
+  return ctx->cev[i];
+}
+
 // run_pipeline (matvec.hpp:233-289) on device buffers, enqueued on ctx->stream.
 // payload_prec >= 0: `in` holds the broadcast payload already in that
-// precision (partition.hpp:198-212); otherwise `in` is double.
+// precision (partition.hpp:198-212); otherwise `in` is double. With `hio`, the
+// host input is copied into `in` chunk by chunk (F) and the output leaves
+// chunk by chunk (F*) on a copy stream, overlapped with the SBGEMV.
 void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5>& p, const void* in,
-              int payload_prec, double* out, cudaEvent_t ev_r2c = nullptr, cudaEvent_t ev_gemv = nullptr) {
+              int payload_prec, double* out, cudaEvent_t ev_r2c = nullptr, cudaEvent_t ev_gemv = nullptr,
+              const HostIO* hio = nullptr) {
   fmv_op* op = const_cast<fmv_op*>(cop);
   const bool fwd = kind == FMV_FORWARD;
   const long nt = (long)op->nt, nb = (long)op->nb();
@@ -626,38 +683,111 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
   const long sx = (n_in + 3) / 4 * 4;
   ctx->x.ensure((size_t)nb * sx * e2 + 256);
   ctx->y.ensure((size_t)nb * n_out * e3 + 256);
-  // Phases 1-2 (+ reorder to TOSI, cast to cfg[2]).
-  if (payload_prec < 0)
-    r2c_dispatch<double>(ctx, p[0], p[1], p[2], static_cast<const double*>(in), nt, 1, n_in, (int)nt, (int)nt,
-                         ctx->x.p, sx, 1);
-  else if (payload_prec == PD)
-    r2c_dispatch<double>(ctx, PD, p[1], p[2], static_cast<const double*>(in), nt, 1, n_in, (int)nt, (int)nt,
-                         ctx->x.p, sx, 1);
-  else if (payload_prec == PS)
-    r2c_dispatch<float>(ctx, PS, p[1], p[2], static_cast<const float*>(in), nt, 1, n_in, (int)nt, (int)nt, ctx->x.p,
-                        sx, 1);
-  else
-    r2c_dispatch<__half>(ctx, PH, p[1], p[2], static_cast<const __half*>(in), nt, 1, n_in, (int)nt, (int)nt,
-                         ctx->x.p, sx, 1);
-  if (ev_r2c) CK(cudaEventRecord(ev_r2c, ctx->stream));
-  // Phase 3 SBGEMV in cfg[2], output cast to cfg[3], TOSI.
   const long m = (long)op->nd, n = (long)op->nm;
-  GemvPlan gp = fwd ? make_gemv(bins, m, n, nb, lda, n * lda, ctx->x.p, sx, ctx->y.p, m)
-                    : make_gemv(bins, m, n, nb, lda, n * lda, ctx->x.p, sx, ctx->y.p, n);
-  const int mode = fwd ? GM_N : GM_C;
-  if (p[2] == PD) {
-    if (p[3] == PD) sbgemv_mode<double2, double2>(ctx, mode, gp, false, nullptr);
-    else sbgemv_mode<double2, float2>(ctx, mode, gp, false, nullptr);
-  } else if (p[2] == PS) {
-    if (p[3] == PD) sbgemv_mode<float2, double2>(ctx, mode, gp, false, nullptr);
-    else sbgemv_mode<float2, float2>(ctx, mode, gp, false, nullptr);
-  } else {
-    if (p[3] == PD) sbgemv_mode<__half2, double2>(ctx, mode, gp, false, nullptr);
-    else sbgemv_mode<__half2, float2>(ctx, mode, gp, false, nullptr);
+  const bool h_in = hio && hio->h_in, h_out = hio && hio->h_out;
+  // Device-resident I/O streams the SBGEMV in one launch; host I/O splits it
+  // into column chunks so the copies hide behind it. (For F the chunk sums
+  // are folded in chunk order, so the two entry points agree to rounding;
+  // each is deterministic.)
+  const std::vector<long> edges = (h_in || h_out) ? chunk_edges(op, p[2], fwd) : std::vector<long>{0, (long)op->nm};
+  const int C = (int)edges.size() - 1;
+  auto chunk_edge = [&](long, int c, int) { return edges[c]; };
+  cudaStream_t cs = ctx->stream;
+  if (C > 16) fail(FMV_EINVAL, "too many chunks");
+  if (h_in || h_out) {  // the copy stream must not run ahead into a buffer still in use
+    CK(cudaEventRecord(chunk_event(ctx, 32), cs));
+    CK(cudaStreamWaitEvent(copy_stream(ctx), chunk_event(ctx, 32), 0));
   }
-  if (ev_gemv) CK(cudaEventRecord(ev_gemv, ctx->stream));
-  // Phases 4-5 (+ reorder back to SOTI, 1/L in cfg[3], unpad, cast cfg[4]).
-  c2r_dispatch(ctx, p[3], p[4], ctx->y.p, n_out, 1, n_out, (int)nt, (int)nt, out, nt);
+
+  // Phases 1-2 (+ reorder to TOSI, cast to cfg[2]) over series [s0, s1).
+  auto r2c_series = [&](long s0, long s1) {
+    void* xo = static_cast<unsigned char*>(ctx->x.p) + s0 * e2;
+    const long cnt = s1 - s0;
+    if (payload_prec < 0)
+      r2c_dispatch<double>(ctx, p[0], p[1], p[2], static_cast<const double*>(in) + s0 * nt, nt, 1, cnt, (int)nt,
+                           (int)nt, xo, sx, 1);
+    else if (payload_prec == PD)
+      r2c_dispatch<double>(ctx, PD, p[1], p[2], static_cast<const double*>(in) + s0 * nt, nt, 1, cnt, (int)nt,
+                           (int)nt, xo, sx, 1);
+    else if (payload_prec == PS)
+      r2c_dispatch<float>(ctx, PS, p[1], p[2], static_cast<const float*>(in) + s0 * nt, nt, 1, cnt, (int)nt, (int)nt,
+                          xo, sx, 1);
+    else
+      r2c_dispatch<__half>(ctx, PH, p[1], p[2], static_cast<const __half*>(in) + s0 * nt, nt, 1, cnt, (int)nt,
+                           (int)nt, xo, sx, 1);
+  };
+  // Phase 3 SBGEMV in cfg[2] over columns [j0, j1), output cast to cfg[3], TOSI.
+  auto gemv_chunk = [&](int c) {
+    const long j0 = chunk_edge(n, c, C), j1 = chunk_edge(n, c + 1, C);
+    const void* A = static_cast<const unsigned char*>(bins) + j0 * lda * (long)e2;
+    GemvPlan gp;
+    if (fwd) {
+      gp = make_gemv(A, m, j1 - j0, nb, lda, n * lda, static_cast<unsigned char*>(ctx->x.p) + j0 * e2, sx, ctx->y.p,
+                     m);
+      ctx->yacc.ensure((size_t)nb * m * 16 + 256);
+      gp.p.yacc = ctx->yacc.p;
+      gp.p.accum = C == 1 ? 0 : c == 0 ? 1 : c == C - 1 ? 3 : 2;
+    } else {
+      gp = make_gemv(A, m, j1 - j0, nb, lda, n * lda, ctx->x.p, sx, static_cast<unsigned char*>(ctx->y.p) + j0 * e3,
+                     n);
+    }
+    run_gemv(ctx, p, fwd ? GM_N : GM_C, gp);
+  };
+  // Phases 4-5 (+ reorder back to SOTI, 1/L in cfg[3], unpad, cast cfg[4]) over series [s0, s1).
+  auto c2r_series = [&](long s0, long s1) {
+    c2r_dispatch(ctx, p[3], p[4], static_cast<unsigned char*>(ctx->y.p) + s0 * e3, n_out, 1, s1 - s0, (int)nt,
+                 (int)nt, out + s0 * nt, nt);
+  };
+
+  if (fwd) {
+    if (h_in) {
+      cudaStream_t ks = copy_stream(ctx);
+      for (int c = 0; c < C; ++c) {
+        const long j0 = chunk_edge(n, c, C), j1 = chunk_edge(n, c + 1, C);
+        CK(cudaMemcpyAsync(const_cast<double*>(static_cast<const double*>(in)) + j0 * nt, hio->h_in + j0 * nt,
+                           (size_t)(j1 - j0) * nt * sizeof(double), cudaMemcpyHostToDevice, ks));
+        CK(cudaEventRecord(chunk_event(ctx, c), ks));
+      }
+      for (int c = 0; c < C; ++c) {
+        CK(cudaStreamWaitEvent(cs, chunk_event(ctx, c), 0));
+        r2c_series(chunk_edge(n, c, C), chunk_edge(n, c + 1, C));
+        gemv_chunk(c);
+      }
+      if (ev_r2c) CK(cudaEventRecord(ev_r2c, cs));
+    } else {
+      r2c_series(0, n_in);
+      if (ev_r2c) CK(cudaEventRecord(ev_r2c, cs));
+      for (int c = 0; c < C; ++c) gemv_chunk(c);
+    }
+    if (ev_gemv) CK(cudaEventRecord(ev_gemv, cs));
+    c2r_series(0, n_out);
+    if (h_out) CK(cudaMemcpyAsync(hio->h_out, out, (size_t)n_out * nt * sizeof(double), cudaMemcpyDeviceToHost, cs));
+  } else {
+    if (h_in)
+      CK(cudaMemcpyAsync(const_cast<double*>(static_cast<const double*>(in)), hio->h_in,
+                         (size_t)n_in * nt * sizeof(double), cudaMemcpyHostToDevice, cs));
+    r2c_series(0, n_in);
+    if (ev_r2c) CK(cudaEventRecord(ev_r2c, cs));
+    if (h_out) {
+      cudaStream_t ks = copy_stream(ctx);
+      for (int c = 0; c < C; ++c) {
+        const long j0 = chunk_edge(n, c, C), j1 = chunk_edge(n, c + 1, C);
+        gemv_chunk(c);
+        c2r_series(j0, j1);
+        CK(cudaEventRecord(chunk_event(ctx, c), cs));
+        CK(cudaStreamWaitEvent(ks, chunk_event(ctx, c), 0));
+        CK(cudaMemcpyAsync(hio->h_out + j0 * nt, out + j0 * nt, (size_t)(j1 - j0) * nt * sizeof(double),
+                           cudaMemcpyDeviceToHost, ks));
+      }
+      CK(cudaEventRecord(chunk_event(ctx, 33), ks));
+      CK(cudaStreamWaitEvent(cs, chunk_event(ctx, 33), 0));
+      if (ev_gemv) CK(cudaEventRecord(ev_gemv, cs));
+    } else {
+      for (int c = 0; c < C; ++c) gemv_chunk(c);
+      if (ev_gemv) CK(cudaEventRecord(ev_gemv, cs));
+      c2r_series(0, n_out);
+    }
+  }
   g_casts.fetch_add(count_casts(p, payload_prec >= 0), std::memory_order_relaxed);
 }
 
@@ -781,9 +911,12 @@ int fmv_ctx_destroy(fmv_ctx* ctx) {
     if (!ctx) return;
     DeviceGuard dg(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    for (auto* b : {&ctx->x, &ctx->y, &ctx->io_in, &ctx->io_out, &ctx->partials, &ctx->counters, &ctx->payload,
-                    &ctx->red})
+    for (auto* b : {&ctx->x, &ctx->y, &ctx->yacc, &ctx->io_in, &ctx->io_out, &ctx->partials, &ctx->counters,
+                    &ctx->payload, &ctx->red})
       b->release();
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    for (auto e : ctx->cev)
+      if (e) cudaEventDestroy(e);
     for (auto& r : ctx->prof) {
       cudaEventDestroy(r.a);
       cudaEventDestroy(r.b);
@@ -955,14 +1088,22 @@ int fmv_matvec(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const 
     double* dout = out;
     cudaStream_t s = ctx->stream;
     auto* te = ctx->te;
-    if (times) CK(cudaEventRecord(te[0], s));
     if (!io_on_device) {
       ctx->io_in.ensure(n_in * sizeof(double));
       ctx->io_out.ensure(n_out * sizeof(double));
-      CK(cudaMemcpyAsync(ctx->io_in.p, in, n_in * sizeof(double), cudaMemcpyHostToDevice, s));
       din = static_cast<const double*>(ctx->io_in.p);
       dout = static_cast<double*>(ctx->io_out.p);
     }
+    if (!io_on_device && !times) {
+      // host I/O: copies overlapped with the SBGEMV of neighbouring column chunks
+      const HostIO hio{in, out};
+      pipeline(ctx, op, kind, p, din, -1, dout, nullptr, nullptr, &hio);
+      CK(cudaStreamSynchronize(s));
+      return;
+    }
+    // timed (PhaseTimings) path: copies serialised so each phase has its own span
+    if (times) CK(cudaEventRecord(te[0], s));
+    if (!io_on_device) CK(cudaMemcpyAsync(ctx->io_in.p, in, n_in * sizeof(double), cudaMemcpyHostToDevice, s));
     if (times) CK(cudaEventRecord(te[1], s));
     pipeline(ctx, op, kind, p, din, -1, dout, times ? te[2] : nullptr, times ? te[3] : nullptr);
     if (times) CK(cudaEventRecord(te[4], s));

@@ -248,6 +248,12 @@ struct GemvParams {
   int LPC;     // (Conj)Trans lanes per column
   void* partials;
   unsigned* counters;
+  // NoTrans column-chunk accumulation (the host splits the n columns into
+  // chunks launched in order): 0 none (y = cast(sum)), 1 first (yacc = sum),
+  // 2 middle (yacc += sum), 3 last (y = cast(yacc + sum)). yacc is [batch][m]
+  // in the accumulator type; the fixed chunk order keeps results deterministic.
+  void* yacc;
+  int accum;
 };
 
 __device__ __forceinline__ long piece_of(long c, long T, int P) {
@@ -427,8 +433,15 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
         const long plo = piece_of(b * p.n, p.T, p.P);
         const long phi = piece_of(b * p.n + p.n - 1, p.T, p.P);
         O* yb = reinterpret_cast<O*>(p.y) + b * p.sy;
+        Acc* ya = reinterpret_cast<Acc*>(p.yacc) + b * p.m;
+        auto emit = [&](int i, Acc v) {
+          if (p.accum == 0) yb[i] = out_cast<O>(v);
+          else if (p.accum == 1) ya[i] = v;
+          else if (p.accum == 2) ya[i] = Tr::add(ya[i], v);
+          else yb[i] = out_cast<O>(Tr::add(ya[i], v));
+        };
         if (plo == phi) {
-          for (int i = t; i < p.m; i += ncons) yb[i] = out_cast<O>(red[i]);
+          for (int i = t; i < p.m; i += ncons) emit(i, red[i]);
         } else {
           Acc* part = reinterpret_cast<Acc*>(p.partials);
           const long slot_id = (long)blockIdx.x + b;
@@ -445,7 +458,7 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
             for (int i = t; i < p.m; i += ncons) {
               Acc v = ldcg(part + (plo + b) * p.m + i);
               for (long pp = plo + 1; pp <= phi; ++pp) v = Tr::add(v, ldcg(part + (pp + b) * p.m + i));
-              yb[i] = out_cast<O>(v);
+              emit(i, v);
             }
             if (t == 0) p.counters[b] = 0u;
           }
@@ -526,7 +539,11 @@ __global__ void k_sbgemv_simple(const GemvParams p) {
     if (o >= p.m) return;
     Acc a = Tr::zero();
     for (long j = 0; j < p.n; ++j) a = Tr::mac(a, Ab[j * p.lda + o], xb[j]);
-    yb[o] = out_cast<O>(a);
+    Acc* ya = reinterpret_cast<Acc*>(p.yacc) + b * p.m;
+    if (p.accum == 0) yb[o] = out_cast<O>(a);
+    else if (p.accum == 1) ya[o] = a;
+    else if (p.accum == 2) ya[o] = Tr::add(ya[o], a);
+    else yb[o] = out_cast<O>(Tr::add(ya[o], a));
   } else {
     if (o >= p.n) return;
     Acc a = Tr::zero();
