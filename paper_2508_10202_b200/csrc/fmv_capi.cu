@@ -539,10 +539,29 @@ bool plan_staged(GemvPlan& gp, int mode, size_t es, size_t accsz, int V) {
     gp.rpt = rpt;
     red = (size_t)p.G * p.m * accsz;
   } else {
-    p.LPC = MV >= 8 ? 8 : 4;
+    // lanes per column: about <= 8 row vectors per lane for short columns,
+    // whole warps (or several warps, combined in shared memory) for tall
+    // ones; widen when a stage holds too few columns to keep 8 warps busy.
+    int lpc = MV <= 16 ? 2 : MV <= 128 ? 8 : MV <= 512 ? 32 : 64;
+    while (lpc >= 32 && lpc < kConsumers && (long)Jc * lpc < kConsumers && lpc * 8 < MV) lpc *= 2;
+    if (lpc > 32) {
+      while (lpc < kConsumers && lpc * 8 < MV) lpc *= 2;
+      while ((long)Jc * lpc < kConsumers && lpc < kConsumers) lpc *= 2;
+    }
+    p.LPC = lpc;
+    red = (size_t)(kConsumers / 32) * accsz;
     gp.block = kConsumers + 32;
   }
-  gp.smem = 512 + (size_t)p.nstage * (p.a_slot + p.x_slot) + (red + 127) / 128 * 128;
+  // (Conj)Trans: keep x_b resident when every batch entry spans >= nstage stages
+  p.xres = 0;
+  p.xres_slot = 0;
+  p.arrive_all = env_int("FMV_SBGEMV_ARRIVE_ALL", 0);
+  if (mode != GM_N && (p.n + Jc - 1) / Jc >= p.nstage && env_int("FMV_SBGEMV_XRES", 1)) {
+    p.xres = 1;
+    p.xres_slot = p.x_slot;
+  }
+  gp.smem = 512 + (size_t)p.nstage * (p.a_slot + (p.xres ? 0 : p.x_slot)) + 2 * (size_t)p.xres_slot +
+            (red + 127) / 128 * 128;
   if (gp.smem > 220 * 1024) return false;
   return true;
 }
@@ -554,8 +573,10 @@ void sbgemv_staged_v(fmv_ctx* ctx, GemvPlan& gp) {
     else if (gp.rpt == 2) sbgemv_launch_t<MODE, E, O, 2, V, 0>(ctx, gp);
     else sbgemv_launch_t<MODE, E, O, 4, V, 0>(ctx, gp);
   } else {
-    if (gp.p.LPC == 8) sbgemv_launch_t<MODE, E, O, 1, V, 8>(ctx, gp);
-    else sbgemv_launch_t<MODE, E, O, 1, V, 4>(ctx, gp);
+    if (gp.p.LPC == 2) sbgemv_launch_t<MODE, E, O, 1, V, 2>(ctx, gp);
+    else if (gp.p.LPC == 8) sbgemv_launch_t<MODE, E, O, 1, V, 8>(ctx, gp);
+    else if (gp.p.LPC == 32) sbgemv_launch_t<MODE, E, O, 1, V, 32>(ctx, gp);
+    else sbgemv_launch_t<MODE, E, O, 1, V, 0>(ctx, gp);  // multi-warp columns
   }
 }
 

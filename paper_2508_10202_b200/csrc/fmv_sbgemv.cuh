@@ -27,6 +27,8 @@
 //    shared-memory reads, xor-shuffle reduction, one store per column.
 #pragma once
 
+#include <type_traits>
+
 #include "fmv_common.cuh"
 
 namespace fmv {
@@ -254,6 +256,13 @@ struct GemvParams {
   // in the accumulator type; the fixed chunk order keeps results deterministic.
   void* yacc;
   int accum;
+  // (Conj)Trans: x_b kept resident in two shared slots (by batch parity),
+  // copied once per batch entry instead of with every stage. Requires every
+  // batch entry to span >= nstage stages (then the slot being refilled is never
+  // still in use).
+  int xres;
+  int xres_slot;
+  int arrive_all;  // every consumer thread arrives on the empty barrier (else one lane per warp)
 };
 
 __device__ __forceinline__ long piece_of(long c, long T, int P) {
@@ -315,6 +324,22 @@ __device__ __forceinline__ VecT<E, V> ldv(const E* p) {
   }
 }
 
+// Neumaier compensated add s += x with compensation c (componentwise).
+__device__ __forceinline__ void neumaier1(float& s, float& c, float x) {
+  const float t = s + x;
+  c += (fabsf(s) >= fabsf(x)) ? ((s - t) + x) : ((x - t) + s);
+  s = t;
+}
+template <class A>
+__device__ __forceinline__ void neumaier_add(A& s, A& c, A x) {
+  if constexpr (std::is_same<A, float2>::value) {
+    neumaier1(s.x, c.x, x.x);
+    neumaier1(s.y, c.y, x.y);
+  } else if constexpr (std::is_same<A, float>::value) {
+    neumaier1(s, c, x);
+  }
+}
+
 template <int MODE, class E, class O, int RPT, int V, int LPC>
 __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
   using Tr = ET<E>;
@@ -325,13 +350,14 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
   uint64_t* empty = full + 16;
   volatile int* s_flag = reinterpret_cast<volatile int*>(sm + 256);
   unsigned char* stages = sm + 512;
-  const int slot = p.a_slot + p.x_slot;
-  Acc* red = reinterpret_cast<Acc*>(stages + (long)p.nstage * slot);
+  const int slot = p.a_slot + (p.xres ? 0 : p.x_slot);
+  unsigned char* xres_base = stages + (long)p.nstage * slot;
+  Acc* red = reinterpret_cast<Acc*>(xres_base + (p.xres ? 2L * p.xres_slot : 0L));
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.nstage; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], ncons / 32);
+      mbar_init(&empty[s], p.arrive_all ? ncons : ncons / 32);
     }
     mbar_fence_init();
   }
@@ -346,10 +372,13 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
     if (threadIdx.x != ncons) return;
     const uint64_t pol_a = policy_evict_first();
     const uint64_t pol_x = policy_evict_last();
+    long prev_b = -1;
     for (SegIter sg(c0, c1, p); sg.more(); sg.advance(p)) {
       sg.load(p);
       const int s = sg.s;
       mbar_wait(&empty[s], sg.par ^ 1u);
+      const bool new_x = !p.xres || sg.b != prev_b;
+      prev_b = sg.b;
       const unsigned char* a0 = p.A + (sg.b * p.sa + sg.j * p.lda) * es;
       const unsigned char* a_lo = reinterpret_cast<const unsigned char*>(reinterpret_cast<uintptr_t>(a0) & ~uintptr_t(15));
       const uintptr_t a_end = reinterpret_cast<uintptr_t>(a0) + (uintptr_t)(((sg.cnt - 1) * p.lda + p.m) * es);
@@ -360,9 +389,10 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
       const uintptr_t x_end = reinterpret_cast<uintptr_t>(x0) + (uintptr_t)(xn * es);
       const uint32_t x_bytes = (uint32_t)(((x_end + 15) & ~uintptr_t(15)) - reinterpret_cast<uintptr_t>(x_lo));
       unsigned char* dst = stages + (long)s * slot;
-      mbar_expect_tx(&full[s], a_bytes + x_bytes);
+      unsigned char* xdst = p.xres ? xres_base + (sg.b & 1) * (long)p.xres_slot : dst + p.a_slot;
+      mbar_expect_tx(&full[s], a_bytes + (new_x ? x_bytes : 0u));
       bulk_g2s(dst, a_lo, a_bytes, &full[s], pol_a);
-      bulk_g2s(dst + p.a_slot, x_lo, x_bytes, &full[s], pol_x);
+      if (new_x) bulk_g2s(xdst, x_lo, x_bytes, &full[s], pol_x);
     }
     return;
   }
@@ -376,11 +406,17 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
     const int r = t % p.RT;
     const int g = t / p.RT;
     const bool active = g < p.G;
-    Acc acc[RPT][V];
+    // fp32 accumulators sum each stage into a fresh partial and fold it into
+    // the running sum with a compensated (Neumaier) add: still fp32
+    // arithmetic (SPEC.md "accumulation precision equals operand precision"),
+    // but the error no longer grows with the ~300 columns a thread visits
+    // per bin. fp64 accumulators use the plain running sum.
+    constexpr bool kComp = !std::is_same<Acc, double2>::value && !std::is_same<Acc, double>::value;
+    Acc acc[RPT][V], cmp[RPT][V];
 #pragma unroll
     for (int q = 0; q < RPT; ++q)
 #pragma unroll
-      for (int v = 0; v < V; ++v) acc[q][v] = Tr::zero();
+      for (int v = 0; v < V; ++v) acc[q][v] = cmp[q][v] = Tr::zero();
     for (SegIter sg(c0, c1, p); sg.more(); sg.advance(p)) {
       sg.load(p);
       const int s = sg.s;
@@ -392,6 +428,11 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
       mbar_wait_sleep(&full[s], sg.par);
       if (active) {
         const int cnt = (int)sg.cnt;
+        Acc part[RPT][V];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q)
+#pragma unroll
+          for (int v = 0; v < V; ++v) part[q][v] = kComp ? Tr::zero() : acc[q][v];
         for (int jj = g; jj < cnt; jj += p.G) {
           const E xv = Xs[jj];
           const E* col = As + (long)jj * p.lda;
@@ -401,13 +442,20 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
             if (vi < MV) {
               const VecT<E, V> a = ldv<E, V>(col + vi * V);
 #pragma unroll
-              for (int v = 0; v < V; ++v) acc[q][v] = Tr::mac(acc[q][v], a.e[v], xv);
+              for (int v = 0; v < V; ++v) part[q][v] = Tr::mac(part[q][v], a.e[v], xv);
             }
           }
         }
+#pragma unroll
+        for (int q = 0; q < RPT; ++q)
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            if constexpr (kComp) neumaier_add(acc[q][v], cmp[q][v], part[q][v]);
+            else acc[q][v] = part[q][v];
+          }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (p.arrive_all || lane == 0) mbar_arrive(&empty[s]);
       if (sg.ends_bin(p)) {
         // ---- flush bin sg.b: intra-CTA reduction over column groups ----
         if (active) {
@@ -416,7 +464,12 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
 #pragma unroll
             for (int v = 0; v < V; ++v) {
               const int row = (r + q * p.RT) * V + v;
-              if (row < p.m) red[(long)g * p.m + row] = acc[q][v];
+              if constexpr (kComp) {
+                if (row < p.m) red[(long)g * p.m + row] = Tr::add(acc[q][v], cmp[q][v]);
+                cmp[q][v] = Tr::zero();
+              } else {
+                if (row < p.m) red[(long)g * p.m + row] = acc[q][v];
+              }
               acc[q][v] = Tr::zero();
             }
           }
@@ -471,11 +524,11 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
     // sees consecutive mbarrier phases); the stage's columns are dealt out
     // CPW at a time across the W warps, LPC lanes per column, 16-byte vector
     // loads, two accumulator chains and a fixed xor-shuffle tree per column.
-    constexpr int CPW = 32 / LPC;
+    constexpr int CPW = LPC > 0 ? 32 / LPC : 1;
     const int W = ncons / 32;
     const int w = t >> 5;
-    const int sub = lane / LPC;
-    const int li = lane - sub * LPC;
+    const int sub = LPC > 0 ? lane / LPC : 0;
+    const int li = LPC > 0 ? lane - sub * LPC : lane;
     const bool ragged = (p.m % V) != 0;
     for (SegIter sg(c0, c1, p); sg.more(); sg.advance(p)) {
       sg.load(p);
@@ -484,41 +537,65 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
       const unsigned char* x0 = p.x + sg.b * p.sx * es;
       const unsigned char* base = stages + (long)s * slot;
       const E* As = reinterpret_cast<const E*>(base + (reinterpret_cast<uintptr_t>(a0) & 15));
-      const E* Xs = reinterpret_cast<const E*>(base + p.a_slot + (reinterpret_cast<uintptr_t>(x0) & 15));
+      const unsigned char* xb = p.xres ? xres_base + (sg.b & 1) * (long)p.xres_slot : base + p.a_slot;
+      const E* Xs = reinterpret_cast<const E*>(xb + (reinterpret_cast<uintptr_t>(x0) & 15));
       O* yb = reinterpret_cast<O*>(p.y) + sg.b * p.sy + sg.j;
       mbar_wait_sleep(&full[s], sg.par);
       const int cnt = (int)sg.cnt;
-      for (int jb = w * CPW; jb < cnt; jb += W * CPW) {
-        const int jj = jb + sub;
-        const bool valid = jj < cnt;
-        Acc a0c = Tr::zero(), a1c = Tr::zero();
-        if (valid) {
-          const E* col = As + (long)jj * p.lda;
-          auto body = [&](Acc& acc, int vi) {
-            const VecT<E, V> a = ldv<E, V>(col + vi * V);
-            const VecT<E, V> x = ldv<E, V>(Xs + vi * V);
+      auto dot = [&](const E* col, int vi, int vstep, Acc& a0c, Acc& a1c) {
+        auto body = [&](Acc& acc, int v0) {
+          const VecT<E, V> a = ldv<E, V>(col + v0 * V);
+          const VecT<E, V> x = ldv<E, V>(Xs + v0 * V);
 #pragma unroll
-            for (int v = 0; v < V; ++v) {
-              if (V == 1 || !ragged || vi * V + v < p.m) {
-                if constexpr (MODE == GM_C) acc = Tr::macc(acc, a.e[v], x.e[v]);
-                else acc = Tr::mac(acc, a.e[v], x.e[v]);
-              }
+          for (int v = 0; v < V; ++v) {
+            if (V == 1 || !ragged || v0 * V + v < p.m) {
+              if constexpr (MODE == GM_C) acc = Tr::macc(acc, a.e[v], x.e[v]);
+              else acc = Tr::mac(acc, a.e[v], x.e[v]);
             }
-          };
-          int vi = li;
-          for (; vi + LPC < MV; vi += 2 * LPC) {
-            body(a0c, vi);
-            body(a1c, vi + LPC);
           }
-          if (vi < MV) body(a0c, vi);
+        };
+        for (; vi + vstep < MV; vi += 2 * vstep) {
+          body(a0c, vi);
+          body(a1c, vi + vstep);
         }
-        Acc a = Tr::add(a0c, a1c);
+        if (vi < MV) body(a0c, vi);
+      };
+      if constexpr (LPC > 0) {
+        for (int jb = w * CPW; jb < cnt; jb += W * CPW) {
+          const int jj = jb + sub;
+          const bool valid = jj < cnt;
+          Acc a0c = Tr::zero(), a1c = Tr::zero();
+          if (valid) dot(As + (long)jj * p.lda, li, LPC, a0c, a1c);
+          Acc a = Tr::add(a0c, a1c);
 #pragma unroll
-        for (int o = LPC >> 1; o > 0; o >>= 1) a = Tr::add(a, Tr::shfl_xor(a, o));
-        if (valid && li == 0) yb[jj] = out_cast<O>(a);
+          for (int o = LPC >> 1; o > 0; o >>= 1) a = Tr::add(a, Tr::shfl_xor(a, o));
+          if (valid && li == 0) yb[jj] = out_cast<O>(a);
+        }
+      } else {
+        // tall columns: WPC warps per column, warp partials combined in
+        // fixed warp order through shared memory
+        const int WPC = p.LPC >> 5;
+        const int CPI = W / WPC;  // columns per iteration
+        const int cs = w / WPC, wi = w - cs * WPC;
+        for (int jb = 0; jb < cnt; jb += CPI) {
+          const int jj = jb + cs;
+          Acc a0c = Tr::zero(), a1c = Tr::zero();
+          if (jj < cnt) dot(As + (long)jj * p.lda, wi * 32 + lane, WPC * 32, a0c, a1c);
+          Acc a = Tr::add(a0c, a1c);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) a = Tr::add(a, Tr::shfl_xor(a, o));
+          if (lane == 0) red[w] = a;
+          bar_consumers(ncons);
+          if (t < CPI && jb + t < cnt) {
+            Acc v = red[t * WPC];
+            for (int k = 1; k < WPC; ++k) v = Tr::add(v, red[t * WPC + k]);
+            yb[jb + t] = out_cast<O>(v);
+          }
+          bar_consumers(ncons);
+        }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (p.arrive_all || lane == 0) mbar_arrive(&empty[s]);
     }
   }
 }

@@ -127,3 +127,19 @@ def test_gemv_spec_examples():
     assert np.array_equal(y, np.array([-1j, -1j]))
     with pytest.raises(ValueError):
         F.gemv_batched(F.GemvMode.NoTrans, "d", 3, 3, 1, 2, 9, np.zeros(9), 3, np.zeros(3), 3)
+
+
+def test_conjtrans_resident_x_matches_per_stage_x(monkeypatch):
+    """x_b resident in shared memory (copied once per batch entry) gives the
+    same bits as re-copying it with every stage, incl. tall columns (multi-warp
+    per column) and pieces that start mid batch."""
+    rng = np.random.default_rng(9)
+    for m, n, b, dt in ((600, 3000, 3, "z"), (1000, 700, 2, "d"), (100, 5000, 4, "c"), (37, 900, 5, "z")):
+        A = _rand(rng, m * n * b, dt)
+        x = _rand(rng, m * b, dt)
+        out = {}
+        for flag in ("0", "1"):
+            monkeypatch.setenv("FMV_SBGEMV_XRES", flag)
+            out[flag], used = F.gemv_batched(F.GemvMode.ConjTrans, dt, m, n, b, m, m * n, A, m, x, n)
+            assert used == 0
+        assert np.array_equal(out["0"], out["1"]), (m, n, b, dt)

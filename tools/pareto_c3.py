@@ -1,0 +1,103 @@
+"""C3: mixed-precision Pareto sweep at C2 shape on one B200 (BASELINE.json configs[2]).
+
+For F and F*: every config (the reference's 32 plus the 'h' fp16 extensions) is
+timed with CUDA events on device-resident I/O (reps per config) and its
+relative L2 error is taken against the GPU 'ddddd' output. The reference
+binary (oracle/_ref) runs each of the 32 configs once on the same inputs to
+give err_ref(cfg) (vs the CPU 'ddddd'); the stated tolerance is
+max(2 * err_ref, 1e-12), 5e-3 for 'h' configs.
+
+  python tools/pareto_c3.py [--reps 20] [--out profiles/pareto_c3_r01]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("MKL_NUM_THREADS", "1")
+import numpy as np
+
+import paper_2508_10202_b200 as F
+
+NM, ND, NT, SEED = 5000, 100, 1000, 20250814
+TAU = 1e-7
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--out", default="profiles/pareto_c3_r01")
+    ap.add_argument("--no-ref", action="store_true")
+    a = ap.parse_args()
+    col = F.non_representable_fill(NM * ND * NT, F.seed_stream(SEED, 0))
+    m = F.non_representable_fill(NM * NT, F.seed_stream(SEED, 1))
+    d = F.non_representable_fill(ND * NT, F.seed_stream(SEED, 2))
+    op = F.setup_operator(F.BlockColumn(F.ProblemDims(NM, ND, NT), col))
+    cfgs = F.enumerate_configs(include_half=True)
+    ref_err = {}
+    ref_time = {}
+    if not a.no_ref:
+        from oracle.oracle import ref
+
+        R = ref()
+        t0 = time.time()
+        rop = R.setup_operator(NM, ND, NT, col)
+        print(f"reference setup {time.time() - t0:.1f}s", flush=True)
+        for kind, x in ((0, m), (1, d)):
+            base = None
+            for c in F.enumerate_configs():
+                cs = c.render()
+                t0 = time.time()
+                out = R.matvec(rop, kind, cs, x)
+                ref_time[(kind, cs)] = time.time() - t0
+                if base is None:
+                    base = out
+                ref_err[(kind, cs)] = 0.0 if cs == "ddddd" else float(np.linalg.norm(out - base) / np.linalg.norm(base))
+            print(f"reference sweep kind {kind} done", flush=True)
+    report = {}
+    md = ["# C3 mixed-precision Pareto sweep on 1 x B200", "",
+          f"Shape Nm={NM}, Nd={ND}, Nt={NT}; non_representable_fill (sweep.hpp:32-46), seed {SEED}; "
+          f"{a.reps} timed reps per config (CUDA events, device-resident I/O), {a.warmup} warm-up. "
+          "err = relative L2 vs the GPU 'ddddd' output; err_ref = the reference binary's error for the same "
+          "config vs its own 'ddddd' (1 thread CPU, MKL FFT); tol = max(2*err_ref, 1e-12), 5e-3 for 'h'.", ""]
+    for kind, x, name in ((F.MatvecKind.Forward, m, "F"), (F.MatvecKind.Adjoint, d, "F*")):
+        rows = F.sweep_operator(op, x, kind, repetitions=a.reps, warmup=a.warmup, configs=cfgs)
+        front = {r.config.render() for r in F.pareto_front(rows)}
+        ref_rows = [r for r in rows if "h" not in r.config.render()]
+        opt = F.optimal_config(ref_rows, TAU).render()
+        opt_all = F.optimal_config(rows, TAU).render()
+        t_dd = rows[0].mean_s
+        tab = []
+        for r in rows:
+            cs = r.config.render()
+            er = ref_err.get((int(kind), cs))
+            tol = 5e-3 if "h" in cs else (max(2 * er, 1e-12) if er is not None else None)
+            tab.append({"config": cs, "mean_s": r.mean_s, "min_s": r.min_s, "max_s": r.max_s, "rel_error": r.rel_error,
+                        "err_ref": er, "tol": tol, "within_tol": (r.rel_error <= tol) if tol is not None else None,
+                        "speedup_vs_ddddd": t_dd / r.mean_s, "pareto": cs in front,
+                        "ref_seconds_1thread": ref_time.get((int(kind), cs))})
+        report[name] = {"rows": tab, "optimal_tau_1e-7_reference_grammar": opt, "optimal_tau_1e-7_with_h": opt_all,
+                        "pareto_front": sorted(front)}
+        md += [f"## {name}", "", f"optimal config at tau=1e-7: **{opt}** ({{d,s}} grammar), **{opt_all}** with fp16 'h'; "
+               f"'ddddd' {t_dd * 1e3:.3f} ms", "",
+               "| config | ms | speedup | rel error | err_ref (CPU) | tol | ok | Pareto |", "|---|---|---|---|---|---|---|---|"]
+        for t in sorted(tab, key=lambda t: t["mean_s"]):
+            er = "-" if t["err_ref"] is None else f"{t['err_ref']:.2e}"
+            tol = "-" if t["tol"] is None else f"{t['tol']:.1e}"
+            ok = "-" if t["within_tol"] is None else ("yes" if t["within_tol"] else "NO")
+            md.append(f"| {t['config']} | {t['mean_s'] * 1e3:.3f} | {t['speedup_vs_ddddd']:.2f} | {t['rel_error']:.2e} | "
+                      f"{er} | {tol} | {ok} | {'*' if t['pareto'] else ''} |")
+        md.append("")
+        print("\n".join(md[-len(tab) - 4:]), flush=True)
+    os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
+    json.dump(report, open(a.out + ".json", "w"), indent=1)
+    open(a.out + ".md", "w").write("\n".join(md) + "\n")
+    bad = [(k, t["config"]) for k, v in report.items() for t in v["rows"] if t["within_tol"] is False]
+    print("configs outside tolerance:", bad)
+
+
+if __name__ == "__main__":
+    main()
