@@ -40,7 +40,7 @@ import ctypes  # noqa: E402
 import numpy as np  # noqa: E402
 
 SEED = 20250814
-NM, ND, NT = 5000, 100, 1000
+NM, ND, NT = 5000, 100, 1000  # C2 (BASELINE.json configs[1]); --workload c5 switches to Nd=600 (configs[4])
 METRIC = "F and F* matvecs/sec at 1/2/4/8 B200; SBGEMV+FFT HBM GB/s vs peak"
 UNIT = "matvecs/s"
 
@@ -178,10 +178,11 @@ def run_reference_arm(args, rank, world):
 
 
 def workload_config(world, cfg):
-    return {"workload": f"C2 FFTMatvec Nm={NM}/GPU Nd={ND} Nt={NT}, cfg {cfg}, step = 1 F + 1 F*",
+    name = "C2" if ND == 100 else "C5"
+    return {"workload": f"{name} FFTMatvec Nm={NM}/GPU Nd={ND} Nt={NT}, cfg {cfg}, step = 1 F + 1 F*",
             "n_m_per_gpu": NM, "n_d": ND, "n_t": NT, "n_m_total": NM * world, "precision_config": cfg,
             "operator_bytes_per_gpu": (NT + 1) * ND * NM * 16,
-            "l2": "inputs larger than L2: the 8.0 GB operator is streamed once per matvec",
+            "l2": f"inputs larger than L2: the {(NT + 1) * ND * NM * 16 / 1e9:.1f} GB operator is streamed once per matvec",
             "parallelism": f"1x{world} column partition" + (" (NCCL all-reduce / broadcast)" if world > 1 else ""),
             "matvec_unit": "one F or F* over an Nm=5000 shard; a distributed matvec on N GPUs = N units"}
 
@@ -364,7 +365,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cfg", default="ddddd")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
+                    help="c2: Nm=5000, Nd=100, Nt=1000 per GPU (default); c5: Nd=600 (48 GB fp64 operator per GPU)")
     args = ap.parse_args()
+    global ND
+    if args.workload == "c5":
+        ND = 600
+        args.no_cpu_baseline = True  # the reference needs ~70 GB host RAM and minutes of setup at C5
     if args.warmup < 3:
         args.warmup = 3
     rank = env_int("RANK", 0)

@@ -516,7 +516,20 @@ constexpr int kConsumers = 256;  // consumer threads per CTA (+1 producer warp);
 bool plan_staged(GemvPlan& gp, int mode, size_t es, size_t accsz, int V) {
   GemvParams& p = gp.p;
   const long col_bytes = p.lda * (long)es;
-  const int a_target = env_int("FMV_SBGEMV_STAGE_BYTES", 32 * 1024);
+  const int MV0 = (p.m + V - 1) / V;
+  int a_target = 32 * 1024;
+  int nst = 3;
+  if (mode != GM_N && MV0 > 128) {
+    // tall (Conj)Trans columns: 64-96 KB stages (>= ~6 columns), one warp per
+    // column, 3 stages when they fit the 227 KB per-CTA limit, else 2, shrunk
+    // until they fit (tools/tune_conjtrans.py)
+    const long xb = ((long)p.m * es + 32 + 127) / 128 * 128 + 128;
+    const long budget = 220 * 1024;
+    a_target = (int)std::min<long>(96 * 1024, std::max<long>(64 * 1024, 6 * col_bytes));
+    nst = 3 * ((long)a_target + 256) + 2 * xb <= budget ? 3 : 2;
+    while (a_target > col_bytes && (long)nst * (a_target + 256) + 2 * xb > budget) a_target -= (int)col_bytes;
+  }
+  a_target = env_int("FMV_SBGEMV_STAGE_BYTES", a_target);
   int Jc = (int)std::max<long>(1, a_target / std::max<long>(col_bytes, 1));
   const long max_a = ((long)(Jc - 1) * p.lda + p.m) * (long)es;
   if (max_a > 96 * 1024) return false;
@@ -525,7 +538,7 @@ bool plan_staged(GemvPlan& gp, int mode, size_t es, size_t accsz, int V) {
   p.a_slot = up128(max_a + 32);
   const long max_x = (mode == GM_N ? (long)Jc : (long)p.m) * (long)es;
   p.x_slot = up128(max_x + 32);
-  p.nstage = std::max(2, std::min(16, env_int("FMV_SBGEMV_STAGES", 3)));
+  p.nstage = std::max(2, std::min(16, env_int("FMV_SBGEMV_STAGES", nst)));
   size_t red = 0;
   const int MV = (p.m + V - 1) / V;
   if (mode == GM_N) {
@@ -542,12 +555,14 @@ bool plan_staged(GemvPlan& gp, int mode, size_t es, size_t accsz, int V) {
     // lanes per column: about <= 8 row vectors per lane for short columns,
     // whole warps (or several warps, combined in shared memory) for tall
     // ones; widen when a stage holds too few columns to keep 8 warps busy.
-    int lpc = MV <= 16 ? 2 : MV <= 128 ? 8 : MV <= 512 ? 32 : 64;
-    while (lpc >= 32 && lpc < kConsumers && (long)Jc * lpc < kConsumers && lpc * 8 < MV) lpc *= 2;
-    if (lpc > 32) {
+    int lpc = MV <= 16 ? 2 : MV <= 128 ? 8 : MV <= 2048 ? 32 : 64;
+    if (lpc > 32) {  // very tall columns: several warps per column
       while (lpc < kConsumers && lpc * 8 < MV) lpc *= 2;
       while ((long)Jc * lpc < kConsumers && lpc < kConsumers) lpc *= 2;
     }
+    const int lpc_env = env_int("FMV_SBGEMV_LPC", 0);
+    if (lpc_env == 2 || lpc_env == 8 || lpc_env == 32 || lpc_env == 64 || lpc_env == 128 || lpc_env == 256)
+      lpc = lpc_env;
     p.LPC = lpc;
     red = (size_t)(kConsumers / 32) * accsz;
     gp.block = kConsumers + 32;
@@ -562,7 +577,7 @@ bool plan_staged(GemvPlan& gp, int mode, size_t es, size_t accsz, int V) {
   }
   gp.smem = 512 + (size_t)p.nstage * (p.a_slot + (p.xres ? 0 : p.x_slot)) + 2 * (size_t)p.xres_slot +
             (red + 127) / 128 * 128;
-  if (gp.smem > 220 * 1024) return false;
+  if (gp.smem > 227 * 1024) return false;
   return true;
 }
 
