@@ -11,7 +11,8 @@ import os
 from ctypes import POINTER, c_char, c_char_p, c_double, c_int, c_size_t, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfftmv_cuda.so")
+# FMV_LIB_PATH: load an alternative build (A/B tuning runs); default is the in-tree library.
+LIB_PATH = os.environ.get("FMV_LIB_PATH") or os.path.join(_HERE, "libfftmv_cuda.so")
 
 FMV_OK, FMV_EINVAL, FMV_ECUDA, FMV_ENCCL, FMV_ENOMEM, FMV_EUNSUPPORTED = 0, 1, 2, 3, 4, 5
 FORWARD, ADJOINT = 0, 1

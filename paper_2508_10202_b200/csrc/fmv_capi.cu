@@ -158,11 +158,16 @@ FftGeom make_geom(int Nt, int nout) {
 
 struct TwiddleCache {
   std::mutex mu;
-  std::map<std::tuple<int, int, int>, void*> tabs;  // (device, L, prec) -> device table
+  // (device, L, prec, RX) -> device table; RX = 0: the base table
+  // exp(-2*pi*i*m/L), m < L; RX > 1: the base table followed by one table per
+  // register-FFT pass p = 2..NP (Ns = RX^(p-1)) laid out [q*Ns + k] =
+  // base[q*k*L/(Ns*RX)], so a warp's twiddle read for fixed q is contiguous
+  // in k (k_r2c_reg / k_c2r_reg); the values are bitwise the base table's.
+  std::map<std::tuple<int, int, int, int>, void*> tabs;
   ~TwiddleCache() {}  // tables live for the process (like the reference's plan cache, fft.hpp:152-164)
-  const void* get(int dev, int L, int prec) {
+  const void* get(int dev, int L, int prec, int RX = 0) {
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(dev, L, prec);
+    auto key = std::make_tuple(dev, L, prec, RX);
     auto it = tabs.find(key);
     if (it != tabs.end()) return it->second;
     // exp(-2*pi*i*m/L), long double, exact at multiples of pi/2
@@ -187,6 +192,18 @@ struct TwiddleCache {
         im[m] = (double)(float)s;
       }
     }
+    if (RX > 1) {
+      const int N = L / 2;
+      for (int Ns = RX; Ns < N; Ns *= RX) {
+        for (int q = 0; q < RX; ++q)
+          for (int k = 0; k < Ns; ++k) {
+            const int m = q * k * (L / (Ns * RX));
+            re.push_back(re[m]);
+            im.push_back(im[m]);
+          }
+      }
+    }
+    L = (int)re.size();
     void* d = nullptr;
     if (prec == PD) {
       std::vector<double2> h(L);
@@ -391,11 +408,51 @@ int fft_lg_series_per_cta(int N, size_t celem) {
   return lg;
 }
 
+// Register-resident FFT kernels (fmv_fft.cuh k_r2c_reg / k_c2r_reg) cover
+// N = 1000 (10^3) and N = 100 (10^2), SOTI <-> TOSI; everything else (and
+// FMV_FFT_LEGACY=1) uses the general mixed-radix kernels.
+bool fft_reg_ok(int N) {
+  return (N == 1000 || N == 100) && env_int("FMV_FFT_LEGACY", 0) == 0;
+}
+
+template <int C0, int C1, int C2, class Tin, int RX, int NP, int S>
+void r2c_reg_launch(fmv_ctx* ctx, const Tin* in, long in_ss, long nseries, int nvalid, void* out, long out_ks) {
+  using R = typename PT<C1>::real;
+  using C = typename CT<R>::c;
+  const int N = RegPlan<RX, NP>::N;
+  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, 2 * N, C1, RX));
+  bool vec = (in_ss % 2 == 0) && (nvalid % 2 == 0);
+  if constexpr (sizeof(Tin) == 8) vec = vec && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  else if constexpr (sizeof(Tin) == 4) vec = vec && (reinterpret_cast<uintptr_t>(in) & 7) == 0;
+  else vec = false;
+  const long grid = (nseries + S - 1) / S;
+  static std::once_flag once;  // static smem only: ask for the max carveout so more CTAs fit per SM
+  std::call_once(once, [] {
+    CK(cudaFuncSetAttribute((const void*)k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>,
+                            cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  });
+  launch(ctx, 0, [&] {
+    k_r2c_reg<C0, C1, C2, Tin, RX, NP, S><<<(unsigned)grid, S * RegPlan<RX, NP>::NR, 0, ctx->stream>>>(
+        in, in_ss, nseries, nvalid, vec, static_cast<typename PT<C2>::cplx*>(out), out_ks, tw);
+  });
+}
+
 template <int C0, int C1, int C2, class Tin>
 void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, int N, int nvalid, void* out,
            long out_ks, long out_ss) {
   using R = typename PT<C1>::real;
   using C = typename CT<R>::c;
+  constexpr bool tin_ok = sizeof(Tin) == 8 || (sizeof(Tin) == 4 && C0 == PS) || (sizeof(Tin) == 2 && C0 == PH);
+  if constexpr (tin_ok) {
+    if (in_ts == 1 && out_ss == 1 && fft_reg_ok(N)) {
+      constexpr bool f64 = sizeof(R) == 8;
+      if (N == 1000)
+        r2c_reg_launch<C0, C1, C2, Tin, 10, 3, f64 ? 2 : 4>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
+      else
+        r2c_reg_launch<C0, C1, C2, Tin, 10, 2, f64 ? 16 : 32>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
+      return;
+    }
+  }
   const FftGeom g = make_geom(N, nvalid);
   const int lgS = fft_lg_series_per_cta(g.N, sizeof(C));
   const int S = 1 << lgS;
@@ -430,10 +487,37 @@ void r2c_dispatch(fmv_ctx* ctx, int c0, int c1, int c2, const Tin* in, long in_s
   fail(FMV_EINVAL, "r2c: unsupported precision combination");
 }
 
+template <int C3, int C4, class Tout, int RX, int NP, int S>
+void c2r_reg_launch(fmv_ctx* ctx, const void* in, long in_ks, long nseries, int nout, Tout* out, long out_ss) {
+  using C = typename PT<C3>::cplx;
+  const int N = RegPlan<RX, NP>::N;
+  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, 2 * N, C3, RX));
+  const bool vec = sizeof(Tout) == 8 && (out_ss % 2 == 0) && (nout % 2 == 0) &&
+                   (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  const long grid = (nseries + S - 1) / S;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    CK(cudaFuncSetAttribute((const void*)k_c2r_reg<C3, C4, Tout, RX, NP, S>,
+                            cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  });
+  launch(ctx, 3, [&] {
+    k_c2r_reg<C3, C4, Tout, RX, NP, S><<<(unsigned)grid, S * RegPlan<RX, NP>::NR, 0, ctx->stream>>>(
+        static_cast<const C*>(in), in_ks, nseries, nout, vec, out, out_ss, tw);
+  });
+}
+
 template <int C3, int C4, class Tout>
 void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, int N, int nout, Tout* out,
            long out_ss) {
   using C = typename PT<C3>::cplx;
+  if (in_ss == 1 && fft_reg_ok(N)) {
+    constexpr bool f64 = C3 == PD;
+    if (N == 1000)
+      c2r_reg_launch<C3, C4, Tout, 10, 3, f64 ? 2 : 4>(ctx, in, in_ks, nseries, nout, out, out_ss);
+    else
+      c2r_reg_launch<C3, C4, Tout, 10, 2, f64 ? 16 : 32>(ctx, in, in_ks, nseries, nout, out, out_ss);
+    return;
+  }
   const FftGeom g = make_geom(N, nout);
   const int lgS = fft_lg_series_per_cta(g.N, sizeof(C));
   const int S = 1 << lgS;

@@ -62,6 +62,10 @@ struct RadixK<double> {
   static constexpr double s51 = 0.95105651629515357211643933337938214;  // sin(2pi/5)
   static constexpr double s52 = 0.58778525229247312916870595463907277;  // sin(4pi/5)
   static constexpr double r2 = 0.70710678118654752440084436210484904;   // sqrt(1/2)
+  static constexpr double c10 = 0.80901699437494742410229341718281906;  // cos(2pi/10)
+  static constexpr double s10 = 0.58778525229247312916870595463907277;  // sin(2pi/10)
+  static constexpr double c16 = 0.92387953251128675612818318939678829;  // cos(2pi/16)
+  static constexpr double s16 = 0.38268343236508977172845998403039887;  // sin(2pi/16)
 };
 template <>
 struct RadixK<float> {
@@ -71,6 +75,10 @@ struct RadixK<float> {
   static constexpr float s51 = 0.95105651629515357211643933337938214f;
   static constexpr float s52 = 0.58778525229247312916870595463907277f;
   static constexpr float r2 = 0.70710678118654752440084436210484904f;
+  static constexpr float c10 = 0.80901699437494742410229341718281906f;
+  static constexpr float s10 = 0.58778525229247312916870595463907277f;
+  static constexpr float c16 = 0.92387953251128675612818318939678829f;
+  static constexpr float s16 = 0.38268343236508977172845998403039887f;
 };
 
 // In-register DFT of size Rn, direction D (-1 forward, +1 inverse).
@@ -106,6 +114,57 @@ __device__ __forceinline__ void butterfly(typename CT<R>::c* v) {
     v[6] = csub(e[2], o2);
     v[3] = cadd(e[3], o3);
     v[7] = csub(e[3], o3);
+  } else if constexpr (Rn == 10) {
+    // 10 = 2 x 5 (Cooley-Tukey): two 5-point DFTs, then X[k] = E[k] + W10^k O[k],
+    // X[k+5] = E[k] - W10^k O[k], W10 = exp(D*2*pi*i/10).
+    C e[5] = {v[0], v[2], v[4], v[6], v[8]};
+    C o[5] = {v[1], v[3], v[5], v[7], v[9]};
+    butterfly<R, D, 5>(e);
+    butterfly<R, D, 5>(o);
+    const R c1 = K::c10, s1 = D * K::s10;  // W10^1 = (cos 36, D sin 36)
+    const R c2 = K::c51, s2 = D * K::s51;  // W10^2 = (cos 72, D sin 72)
+    const C t1 = {c1 * o[1].x - s1 * o[1].y, c1 * o[1].y + s1 * o[1].x};
+    const C t2 = {c2 * o[2].x - s2 * o[2].y, c2 * o[2].y + s2 * o[2].x};
+    const C t3 = {-c2 * o[3].x - s2 * o[3].y, -c2 * o[3].y + s2 * o[3].x};  // W10^3 = (-cos 72, D sin 72)
+    const C t4 = {-c1 * o[4].x - s1 * o[4].y, -c1 * o[4].y + s1 * o[4].x};  // W10^4 = (-cos 36, D sin 36)
+    v[0] = cadd(e[0], o[0]);
+    v[5] = csub(e[0], o[0]);
+    v[1] = cadd(e[1], t1);
+    v[6] = csub(e[1], t1);
+    v[2] = cadd(e[2], t2);
+    v[7] = csub(e[2], t2);
+    v[3] = cadd(e[3], t3);
+    v[8] = csub(e[3], t3);
+    v[4] = cadd(e[4], t4);
+    v[9] = csub(e[4], t4);
+  } else if constexpr (Rn == 16) {
+    // 16 = 4 x 4: four 4-point DFTs on the decimated inputs, twiddles W16^(a*b), four more.
+    C a[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) a[r][c] = v[c * 4 + r];
+      butterfly<R, D, 4>(a[r]);
+    }
+    // a[r][k1] *= W16^(r*k1)
+    const R cs8 = K::r2, c16 = K::c16, s16 = K::s16;
+    auto rot = [&](C x, R c, R s) { return C{c * x.x - D * s * x.y, c * x.y + D * s * x.x}; };
+    a[1][1] = rot(a[1][1], c16, s16);
+    a[1][2] = rot(a[1][2], cs8, cs8);
+    a[1][3] = rot(a[1][3], s16, c16);
+    a[2][1] = rot(a[2][1], cs8, cs8);
+    a[2][2] = cmuli<D>(a[2][2]);
+    a[2][3] = rot(a[2][3], -cs8, cs8);
+    a[3][1] = rot(a[3][1], s16, c16);
+    a[3][2] = rot(a[3][2], -cs8, cs8);
+    a[3][3] = rot(a[3][3], -c16, -s16);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      C b[4] = {a[0][k1], a[1][k1], a[2][k1], a[3][k1]};
+      butterfly<R, D, 4>(b);
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = b[k2];
+    }
   } else if constexpr (Rn == 3) {
     const C t = cadd(v[1], v[2]);
     const C u = csub(v[1], v[2]);
@@ -411,6 +470,312 @@ __global__ void __launch_bounds__(256) k_c2r(const typename PT<C3>::cplx* __rest
     const int s = g.nout_div.div(e), t = e - s * nout;
     const C v = z[s * ss + (t >> 1)];
     out[(s0 + s) * out_ss + t] = (Tout)rnd<C4>((double)((t & 1) ? v.y : v.x));
+  }
+}
+
+// ======================================================================
+// Register-resident kernels for N = RX^NP (N = 1000 = 10^3, 100 = 10^2,
+// 256 = 16^2, 4096 = 16^3, 512 = 8^3 ...): the matvec hot path.
+//
+// Each thread owns ONE radix-RX butterfly per pass (T = S * N/RX threads for
+// S series), so a pass is: read RX values, twiddle, DFT-RX in registers,
+// barrier, write in place, barrier -- one shared-memory round trip per pass
+// instead of a ping-pong buffer per radix-2/4/8/5 stage. The r2c first pass
+// reads straight from global memory (the pass-1 Stockham read pattern
+// z[j + q*N/RX] is contiguous across j) and the c2r last pass writes straight
+// to global memory (its write pattern z[j + q*N/RX] is contiguous too), so
+// r2c costs NP smem round trips + the bin post-pass and c2r the bin pre-pass
+// + NP - 1. Twiddles are index-exact table reads (the table of
+// exp(-2*pi*i*m/L) the legacy kernel uses), so both kernels compute the same
+// DFT; summation order differs (radix-10 vs 8/5 stages), rounding-level.
+// ======================================================================
+template <int RX, int NP>
+struct RegPlan {
+  static constexpr int N = NP == 2 ? RX * RX : RX * RX * RX;
+  static constexpr int NR = N / RX;  // butterflies per series per pass
+};
+
+// Shared series stride: N rounded up so consecutive series start 128/S bytes
+// apart modulo 128 (at least one element): the S-interleaved post/pre-pass
+// (thread e -> bin e/S, series e%S) then spreads over distinct banks.
+template <class C, int N, int S>
+constexpr int reg_series_stride() {
+  constexpr int E = (int)sizeof(C);
+  constexpr int per128 = 128 / E;                        // elements per 128 B
+  constexpr int off = (128 / S > E ? 128 / S : E) / E;   // target offset in elements
+  int ss = N;
+  while (ss % per128 != off % per128) ++ss;
+  return ss;
+}
+
+// One Stockham pass with Ns > 1 over the thread's butterfly: read, twiddle,
+// DFT, barrier, write, barrier.
+// Offset of pass Ns's twiddle table [q*Ns + k] behind the 2N-entry base table.
+template <int RX, int N, int Ns>
+constexpr int reg_tw_offset() {
+  int off = 2 * N;
+  for (int ns = RX; ns < Ns; ns *= RX) off += RX * ns;
+  return off;
+}
+
+// v[q] *= w^(q*k), q = 1..RX-1, from the pass table twp[q*Ns + k]. For
+// RX = 10 only q = 1, 2, 3, 6 are read and the rest formed as one product of
+// two table values (w4 = w1 w3, w5 = w2 w3, w7 = w1 w6, w8 = w2 w6,
+// w9 = w3 w6: ~1 ulp), cutting the L1 twiddle traffic that bounds the pass.
+template <class R, int D, int RX, int Ns>
+__device__ __forceinline__ void apply_twiddles(typename CT<R>::c* v, const typename CT<R>::c* __restrict__ twp, int k) {
+  if constexpr (RX == 10) {
+    const auto w1 = twiddle<D>(twp, Ns + k), w2 = twiddle<D>(twp, 2 * Ns + k);
+    const auto w3 = twiddle<D>(twp, 3 * Ns + k), w6 = twiddle<D>(twp, 6 * Ns + k);
+    v[1] = cmul(v[1], w1);
+    v[2] = cmul(v[2], w2);
+    v[3] = cmul(v[3], w3);
+    v[4] = cmul(v[4], cmul(w1, w3));
+    v[5] = cmul(v[5], cmul(w2, w3));
+    v[6] = cmul(v[6], w6);
+    v[7] = cmul(v[7], cmul(w1, w6));
+    v[8] = cmul(v[8], cmul(w2, w6));
+    v[9] = cmul(v[9], cmul(w3, w6));
+  } else {
+#pragma unroll
+    for (int q = 1; q < RX; ++q) v[q] = cmul(v[q], twiddle<D>(twp, q * Ns + k));
+  }
+}
+
+// exp(-i*pi*q/10), q = 0..9 (the c2r pre-pass factor w^(q*N/10) for L = 2N).
+template <class R>
+__device__ __forceinline__ typename CT<R>::c half_turn10(int q) {
+  using K = RadixK<R>;
+  const R cs[10] = {R(1), K::s51, K::c10, K::s10, K::c51, R(0), -K::c51, -K::s10, -K::c10, -K::s51};
+  const R sn[10] = {R(0), K::c51, K::s10, K::c10, K::s51, R(1), K::s51, K::c10, K::s10, K::c51};
+  return {cs[q], -sn[q]};
+}
+
+// Shared-memory position of logical element i (identity: a pad-every-RX
+// layout was measured to trade write conflicts for more read conflicts).
+template <int RX>
+__host__ __device__ constexpr int pidx(int i) {
+  return i;
+}
+
+// Pass-1 store o[q] = v[q], q < RX, for thread j at o = buf + j*RX. With
+// 16-byte elements and even RX, lanes t and t+4 of a quarter-warp would hit
+// the same bank group for every q; lanes with (t>>2)&1 store the pair q^1
+// first, which spreads the quarter over all 8 groups.
+template <int RX, class C>
+__device__ __forceinline__ void store_stride_rx(C* o, const C* v) {
+  if constexpr (RX % 2 == 0 && sizeof(C) == 16) {
+    const int d = (threadIdx.x >> 2) & 1;
+#pragma unroll
+    for (int q = 0; q < RX; ++q) o[q ^ d] = d ? v[q ^ 1] : v[q];
+  } else {
+#pragma unroll
+    for (int q = 0; q < RX; ++q) o[q] = v[q];
+  }
+}
+
+template <class R, int D, int RX, int N, int Ns>
+__device__ __forceinline__ void reg_pass(typename CT<R>::c* __restrict__ buf, int j, bool act,
+                                         const typename CT<R>::c* __restrict__ tw) {
+  using C = typename CT<R>::c;
+  constexpr int NR = N / RX;
+  const C* __restrict__ twp = tw + reg_tw_offset<RX, N, Ns>();
+  C v[RX];
+  const int k = j % Ns;
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < RX; ++q) v[q] = buf[pidx<RX>(j + q * NR)];
+    apply_twiddles<R, D, RX, Ns>(v, twp, k);
+    butterfly<R, D, RX>(v);
+  }
+  __syncthreads();
+  if (act) {
+    const int o = (j - k) * RX + k;
+#pragma unroll
+    for (int q = 0; q < RX; ++q) buf[pidx<RX>(o + q * Ns)] = v[q];
+  }
+  __syncthreads();
+}
+
+template <int I, int RX>
+struct IPow {
+  static constexpr int v = RX * IPow<I - 1, RX>::v;
+};
+template <int RX>
+struct IPow<0, RX> {
+  static constexpr int v = 1;
+};
+
+// Phases 1-2 + reorder (as k_r2c) for SOTI input in[s*in_ss + t] and TOSI
+// output out[k*out_ks + s]; S series per CTA.
+template <int C0, int C1, int C2, class Tin, int RX, int NP, int S>
+__global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::NR <= 256 ? 4 : 2)
+    k_r2c_reg(const Tin* __restrict__ in, long in_ss, long nseries, int nvalid, bool vec,
+              typename PT<C2>::cplx* __restrict__ out, long out_ks,
+              const typename CT<typename PT<C1>::real>::c* __restrict__ tw) {
+  using R = typename PT<C1>::real;
+  using C = typename CT<R>::c;
+  using OutC = typename PT<C2>::cplx;
+  constexpr int N = RegPlan<RX, NP>::N, NR = RegPlan<RX, NP>::NR, T = S * NR;
+  constexpr int SS = reg_series_stride<C, pidx<RX>(N - 1) + 1, S>();
+  __shared__ __align__(16) C sbuf[S * SS];
+  const int s = threadIdx.x / NR, j = threadIdx.x - s * NR;
+  const long s0 = (long)blockIdx.x * S;
+  const int ns = (int)min((long)S, nseries - s0);
+  const bool act = s < ns;
+  C* buf = sbuf + s * SS;
+
+  // Pass 1 (Ns = 1, no twiddles): z[n] = v[2n] + i v[2n+1], n = j + q*NR.
+  {
+    C v[RX];
+    const Tin* p = in + (s0 + s) * in_ss;
+#pragma unroll
+    for (int q = 0; q < RX; ++q) {
+      const int n = j + q * NR;
+      const int t0 = 2 * n;
+      v[q] = C{R(0), R(0)};
+      if (act && t0 < nvalid) {
+        if constexpr (sizeof(Tin) == 8) {
+          if (vec) {
+            const double2 pr = __ldg(reinterpret_cast<const double2*>(p) + n);
+            v[q] = C{(R)rnd<C0>(pr.x), (R)rnd<C0>(pr.y)};
+            continue;
+          }
+        } else if constexpr (sizeof(Tin) == 4) {
+          if (vec) {
+            const float2 pr = __ldg(reinterpret_cast<const float2*>(p) + n);
+            v[q] = C{(R)rnd<C0>((double)pr.x), (R)rnd<C0>((double)pr.y)};
+            continue;
+          }
+        }
+        const R a = (R)rnd<C0>(to_d(p[t0]));
+        const R b = t0 + 1 < nvalid ? (R)rnd<C0>(to_d(p[t0 + 1])) : R(0);
+        v[q] = C{a, b};
+      }
+    }
+    butterfly<R, -1, RX>(v);
+    if (act) store_stride_rx<RX>(buf + j * RX, v);
+    __syncthreads();
+  }
+  if constexpr (NP >= 3) reg_pass<R, -1, RX, N, RX>(buf, j, act, tw);
+  if constexpr (NP == 2) reg_pass<R, -1, RX, N, RX>(buf, j, act, tw);
+  else reg_pass<R, -1, RX, N, RX * RX>(buf, j, act, tw);
+
+  // Post-pass: X[k] = E[k] + w^k (-i) D[k] with E, D from Z[k] and
+  // conj Z[N-k]. Bins k and N-k (k = 0 pairs with N) share the two loads.
+  // Consecutive threads take consecutive series of one bin pair (S-element
+  // contiguous TOSI runs).
+  const R half = R(0.5);
+  auto post = [&](C A, C B, int k) {  // B = conj(Z[N-k])
+    const C E = {(A.x + B.x) * half, (A.y + B.y) * half};
+    const C Dm = {(A.x - B.x) * half, (A.y - B.y) * half};
+    return cadd(E, cmul(__ldg(tw + k), cmuli<-1>(Dm)));
+  };
+  for (int e = threadIdx.x; e < S * (N / 2 + 1); e += T) {
+    const int k = e / S, si = e - k * S;
+    if (si >= ns) continue;
+    const C* Z = sbuf + si * SS;
+    const int kp = k == 0 ? N : N - k;
+    const C A1 = Z[pidx<RX>(k)];
+    const C A2 = Z[pidx<RX>(k == 0 ? 0 : N - k)];
+    out[(long)k * out_ks + s0 + si] = cfrom_d<OutC>(to_cd(post(A1, cconj(A2), k)));
+    if (kp != k) out[(long)kp * out_ks + s0 + si] = cfrom_d<OutC>(to_cd(post(A2, cconj(A1), kp)));
+  }
+}
+
+// Phases 4-5 + reorder (as k_c2r) for TOSI input in[k*in_ks + s] and SOTI
+// output out[s*out_ss + t], t < nout; S series per CTA.
+template <int C3, int C4, class Tout, int RX, int NP, int S>
+__global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::NR <= 256 ? 4 : 2)
+    k_c2r_reg(const typename PT<C3>::cplx* __restrict__ in, long in_ks, long nseries, int nout, bool vec,
+              Tout* __restrict__ out, long out_ss, const typename PT<C3>::cplx* __restrict__ tw) {
+  using R = typename PT<C3>::real;
+  using C = typename CT<R>::c;
+  constexpr int N = RegPlan<RX, NP>::N, NR = RegPlan<RX, NP>::NR, T = S * NR;
+  constexpr int SS = reg_series_stride<C, pidx<RX>(N) + 1, S>();
+  __shared__ __align__(16) C sbuf[S * SS];
+  const int s = threadIdx.x / NR, j = threadIdx.x - s * NR;
+  const long s0 = (long)blockIdx.x * S;
+  const int ns = (int)min((long)S, nseries - s0);
+  const bool act = s < ns;
+  C* buf = sbuf + s * SS;
+  const R inv_len = R(1) / (R)(2 * N);
+
+  // Load the N+1 bins of S series (bin-major runs of S), scale by 1/L in the
+  // working precision, drop Im of DC and Nyquist (fft.hpp:130-148).
+  {
+    constexpr int TOT = S * (N + 1);
+    constexpr int U = (TOT + T - 1) / T;
+    C v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = threadIdx.x + u * T;
+      const int k = e / S, si = e - k * S;
+      if (e < TOT && si < ns) v[u] = in[(long)k * in_ks + s0 + si];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = threadIdx.x + u * T;
+      const int k = e / S, si = e - k * S;
+      if (e < TOT && si < ns) {
+        C X = v[u];
+        X.x = X.x * inv_len;
+        X.y = (k == 0 || k == N) ? R(0) : X.y * inv_len;
+        sbuf[si * SS + pidx<RX>(k)] = X;
+      }
+    }
+  }
+  __syncthreads();
+  // Pre-pass fused into pass 1: Z[n] = (X[n] + conj X[N-n]) + i w^-n (X[n] - conj X[N-n]).
+  {
+    C v[RX];
+    if (act) {
+      const C wj = __ldg(tw + j);
+#pragma unroll
+      for (int q = 0; q < RX; ++q) {
+        const int n = j + q * NR;
+        const C A = buf[pidx<RX>(n)];
+        const C B = cconj(buf[pidx<RX>(N - n)]);
+        C w;  // w^n = w^j * w^(q*N/RX); for RX = 10 the second factor is a constant
+        if constexpr (RX == 10) w = q == 0 ? wj : cmul(wj, half_turn10<R>(q));
+        else w = __ldg(tw + n);
+        v[q] = cadd(cadd(A, B), cmuli<1>(cmul(C{w.x, -w.y}, csub(A, B))));
+      }
+      butterfly<R, 1, RX>(v);
+    }
+    __syncthreads();
+    if (act) store_stride_rx<RX>(buf + j * RX, v);
+    __syncthreads();
+  }
+  if constexpr (NP >= 3) reg_pass<R, 1, RX, N, RX>(buf, j, act, tw);
+  // Last pass (Ns = N/RX): out index j + q*NR, straight to global.
+  {
+    constexpr int Ns = NR;
+    const C* __restrict__ twp = tw + reg_tw_offset<RX, N, Ns>();
+    C v[RX];
+    if (act) {
+#pragma unroll
+      for (int q = 0; q < RX; ++q) v[q] = buf[pidx<RX>(j + q * NR)];
+      apply_twiddles<R, 1, RX, Ns>(v, twp, j);
+      butterfly<R, 1, RX>(v);
+      Tout* p = out + (s0 + s) * out_ss;
+#pragma unroll
+      for (int q = 0; q < RX; ++q) {
+        const int n = j + q * NR;
+        const int t0 = 2 * n;
+        if (t0 >= nout) continue;
+        const Tout a = (Tout)rnd<C4>((double)v[q].x);
+        const Tout b = (Tout)rnd<C4>((double)v[q].y);
+        if constexpr (sizeof(Tout) == 8) {
+          if (vec) {
+            reinterpret_cast<double2*>(p)[n] = make_double2(a, b);
+            continue;
+          }
+        }
+        p[t0] = a;
+        if (t0 + 1 < nout) p[t0 + 1] = b;
+      }
+    }
   }
 }
 
