@@ -629,6 +629,8 @@ bool plan_staged(GemvPlan& gp, int mode, size_t es, size_t accsz, int V) {
     int rpt = 1;
     while ((MV + rpt - 1) / rpt > kConsumers) rpt *= 2;
     if (rpt > 4) return false;
+    const int rpt_env = env_int("FMV_SBGEMV_RPT", 0);
+    if ((rpt_env == 2 || rpt_env == 4) && rpt_env > rpt) rpt = rpt_env;
     p.RT = (MV + rpt - 1) / rpt;
     p.G = std::max(1, kConsumers / p.RT);
     const int ncons = (p.RT * p.G + 31) / 32 * 32;

@@ -428,12 +428,40 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
       mbar_wait_sleep(&full[s], sg.par);
       if (active) {
         const int cnt = (int)sg.cnt;
-        Acc part[RPT][V];
+        // Two column chains (columns jj and jj + G) with their own partial
+        // sums, both loads issued before either MAC, so a warp's LDS latency
+        // and FMA dependency chain are paid once per two columns; the chains
+        // are added once per stage (fixed order: deterministic).
+        Acc part[RPT][V], part2[RPT][V];
 #pragma unroll
         for (int q = 0; q < RPT; ++q)
 #pragma unroll
-          for (int v = 0; v < V; ++v) part[q][v] = kComp ? Tr::zero() : acc[q][v];
-        for (int jj = g; jj < cnt; jj += p.G) {
+          for (int v = 0; v < V; ++v) {
+            part[q][v] = kComp ? Tr::zero() : acc[q][v];
+            part2[q][v] = Tr::zero();
+          }
+        const int G = p.G;
+        int jj = g;
+        constexpr bool kTwo = RPT * V <= 4;  // register budget (wide RPT*V variants keep one chain)
+        if constexpr (kTwo) for (; jj + G < cnt; jj += 2 * G) {
+          const E xv0 = Xs[jj], xv1 = Xs[jj + G];
+          const E* col0 = As + (long)jj * p.lda;
+          const E* col1 = col0 + (long)G * p.lda;
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) {
+            const int vi = r + q * p.RT;
+            if (vi < MV) {
+              const VecT<E, V> a0 = ldv<E, V>(col0 + vi * V);
+              const VecT<E, V> a1 = ldv<E, V>(col1 + vi * V);
+#pragma unroll
+              for (int v = 0; v < V; ++v) {
+                part[q][v] = Tr::mac(part[q][v], a0.e[v], xv0);
+                part2[q][v] = Tr::mac(part2[q][v], a1.e[v], xv1);
+              }
+            }
+          }
+        }
+        for (; jj < cnt; jj += G) {
           const E xv = Xs[jj];
           const E* col = As + (long)jj * p.lda;
 #pragma unroll
@@ -450,8 +478,9 @@ __global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
         for (int q = 0; q < RPT; ++q)
 #pragma unroll
           for (int v = 0; v < V; ++v) {
-            if constexpr (kComp) neumaier_add(acc[q][v], cmp[q][v], part[q][v]);
-            else acc[q][v] = part[q][v];
+            const Acc sum = Tr::add(part[q][v], part2[q][v]);
+            if constexpr (kComp) neumaier_add(acc[q][v], cmp[q][v], sum);
+            else acc[q][v] = sum;
           }
       }
       __syncwarp();
