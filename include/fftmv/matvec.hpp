@@ -111,4 +111,42 @@ inline MatvecResult adjoint_matvec(const SpectralOperator& op, const BlockVector
   return {BlockVector::time_double(op.dims.n_m, op.dims.n_t, std::move(out)), t};
 }
 
+// Block (multi-RHS) matvecs -- an addition to the reference API (SURVEY.md §8
+// f2; the Hessian-assembly use case): one call applies F or
+// F* to every vector in `in`, streaming the operator once per 8 (F) / 4 (F*)
+// right-hand sides (fmv_matvec_block). out[r] equals forward_matvec /
+// adjoint_matvec of in[r] up to summation order.
+namespace detail {
+inline std::vector<BlockVector> matvec_block(const SpectralOperator& op, const std::vector<BlockVector>& in,
+                                             PrecisionConfig cfg, bool fwd) {
+  const std::size_t n_in = (fwd ? op.dims.n_m : op.dims.n_d) * op.dims.n_t;
+  const std::size_t n_out = (fwd ? op.dims.n_d : op.dims.n_m) * op.dims.n_t;
+  std::vector<double> packed;
+  packed.reserve(in.size() * n_in);
+  for (const auto& v : in) {
+    check_matvec_input(op, v, fwd);
+    packed.insert(packed.end(), v.f64.begin(), v.f64.end());
+  }
+  std::vector<double> out(in.size() * n_out);
+  if (!in.empty())
+    check(fmv_matvec_block(thread_ctx(), op.handle(), fwd ? FMV_FORWARD : FMV_ADJOINT, cfg.render().c_str(),
+                           in.size(), packed.data(), out.data(), 0));
+  std::vector<BlockVector> res;
+  res.reserve(in.size());
+  for (std::size_t r = 0; r < in.size(); ++r)
+    res.push_back(BlockVector::time_double(fwd ? op.dims.n_d : op.dims.n_m, op.dims.n_t,
+                                           std::vector<double>(out.begin() + r * n_out, out.begin() + (r + 1) * n_out)));
+  return res;
+}
+}  // namespace detail
+
+inline std::vector<BlockVector> forward_matvec_block(const SpectralOperator& op, const std::vector<BlockVector>& m,
+                                                     PrecisionConfig cfg = {}) {
+  return detail::matvec_block(op, m, cfg, true);
+}
+inline std::vector<BlockVector> adjoint_matvec_block(const SpectralOperator& op, const std::vector<BlockVector>& d,
+                                                     PrecisionConfig cfg = {}) {
+  return detail::matvec_block(op, d, cfg, false);
+}
+
 }  // namespace fftmv

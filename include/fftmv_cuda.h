@@ -96,6 +96,21 @@ int fmv_matvec(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const 
 /* Non-blocking variant: device pointers only, enqueued on the ctx stream. */
 int fmv_matvec_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* d_in, double* d_out);
 
+/* ---- block (multi-RHS) matvec: SURVEY.md §8 f2 ----
+ * nrhs independent inputs back to back (nrhs SOTI vectors of n_in*nt
+ * doubles; n_in = nm for FORWARD, nd for ADJOINT), outputs likewise. Each
+ * RHS goes through the same 5-phase pipeline and precision config as
+ * fmv_matvec; the per-bin SBGEMV handles up to 8 RHS per operator pass
+ * (the operator is read from HBM once per 8 RHS instead of once per RHS).
+ * Per-RHS results equal fmv_matvec's up to summation order (fp64: ~1e-15
+ * relative). 'h' SBGEMV configs and FORWARD with nd > 256 run as nrhs
+ * single-RHS pipelines. Blocking; host pointers unless io_on_device. */
+int fmv_matvec_block(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, size_t nrhs, const double* in,
+                     double* out, int io_on_device);
+/* Non-blocking variant: device pointers only, enqueued on the ctx stream. */
+int fmv_matvec_block_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, size_t nrhs, const double* d_in,
+                           double* d_out);
+
 /* ---- batched real FFTs (fft.hpp:110-148), device pointers ----
  * r2c: batch contiguous series of L reals -> batch x (L/2+1) complex bins,
  *      unnormalized, sign -1. c2r: the true inverse, 1/L folded in by

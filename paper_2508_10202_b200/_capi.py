@@ -57,6 +57,8 @@ def lib() -> ctypes.CDLL:
         "fmv_op_device_bytes": (c_size_t, [c_void_p]),
         "fmv_matvec": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_void_p, c_void_p, c_int, POINTER(PhaseTimesC)]),
         "fmv_matvec_async": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_void_p, c_void_p]),
+        "fmv_matvec_block": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_size_t, c_void_p, c_void_p, c_int]),
+        "fmv_matvec_block_async": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_size_t, c_void_p, c_void_p]),
         "fmv_casts_performed": (c_uint64, []),
         "fmv_reset_cast_counter": (None, []),
         "fmv_sbgemv": (c_int, [c_void_p, c_int, c_char, c_size_t, c_size_t, c_size_t, c_size_t, c_size_t, c_void_p,
@@ -89,6 +91,7 @@ def exported_symbols() -> list[str]:
         "fmv_matvec", "fmv_matvec_async", "fmv_casts_performed", "fmv_reset_cast_counter", "fmv_sbgemv",
         "fmv_comm_unique_id", "fmv_comm_init", "fmv_comm_destroy", "fmv_matvec_partitioned", "fmv_seed_stream",
         "fmv_uniform_fill", "fmv_non_representable_fill", "fmv_relative_error", "fmv_fft_r2c", "fmv_fft_c2r",
+        "fmv_matvec_block", "fmv_matvec_block_async",
     ]
 
 

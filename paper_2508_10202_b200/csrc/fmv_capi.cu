@@ -25,6 +25,7 @@
 #include "fmv_common.cuh"
 #include "fmv_fft.cuh"
 #include "fmv_sbgemv.cuh"
+#include "fmv_sbgemm_block.cuh"
 
 using namespace fmv;
 
@@ -913,6 +914,142 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
   g_casts.fetch_add(count_casts(p, payload_prec >= 0), std::memory_order_relaxed);
 }
 
+// ------------------------------------------------- block (multi-RHS) ----
+// K right-hand sides through one pipeline, the per-bin
+// SBGEMV replaced by the block kernel (fmv_sbgemm_block.cuh) that streams the
+// operator once for up to kBlockMax RHS.
+// RHS per block-SBGEMV launch (measured at C2, tools/bench_block.py): F
+// gains up to 8 (3.6x per-RHS throughput at fp64), F* peaks at 4 (2.6x).
+constexpr int kBlockMax = 8;
+inline int block_max(bool fwd) { return fwd ? kBlockMax : 4; }
+
+// Stage plan for k_sbgemm_block: ~32 KB of columns per stage, shrunk until
+// two CTAs fit an SM; false if the shape is outside the kernel's limits.
+bool plan_block(GemvPlan& gp, int mode, size_t es, size_t accsz, int KR) {
+  GemvParams& p = gp.p;
+  if (p.m < 1 || (mode == GM_N && p.m > kConsumers)) return false;
+  auto up128 = [](long v) { return (int)((v + 127) / 128 * 128); };
+  const long col_bytes = std::max<long>(1, p.lda * (long)es);
+  const long budget = 110 * 1024;
+  p.nstage = 3;
+  int Jc = (int)std::max<long>(1, 32768 / col_bytes);
+  size_t red = 0;
+  if (mode == GM_N) {
+    p.RT = p.m;
+    p.G = std::max(1, kConsumers / p.RT);
+    gp.block = (p.RT * p.G + 31) / 32 * 32 + 32;
+  } else {
+    gp.block = kConsumers + 32;
+  }
+  for (;;) {
+    const long max_a = ((long)(Jc - 1) * p.lda + p.m) * (long)es;
+    p.Jc = Jc;
+    p.a_slot = up128(max_a + 32);
+    p.xr_slot = up128((mode == GM_N ? (long)Jc : (long)p.m) * (long)es + 32);
+    p.xres = mode != GM_N && (p.n + Jc - 1) / Jc >= p.nstage;
+    p.xres_slot = 0;
+    red = mode == GM_N ? (size_t)p.G * KR * p.m * accsz : 0;
+    const long xs = (long)KR * p.xr_slot;
+    gp.smem = 512 + (size_t)p.nstage * (p.a_slot + (p.xres ? 0 : xs)) + (p.xres ? 2 * xs : 0) + (red + 127) / 128 * 128;
+    if ((long)gp.smem <= budget || Jc == 1) break;
+    Jc = std::max(1, Jc * 3 / 4);
+  }
+  p.arrive_all = 0;
+  return gp.smem <= 227 * 1024 && (long)(p.Jc - 1) * p.lda * (long)es + p.m * (long)es <= 96 * 1024;
+}
+
+template <int MODE, class E, class O, int KR, int LPC>
+void sbgemm_block_launch_t(fmv_ctx* ctx, GemvPlan& gp) {
+  auto kern = k_sbgemm_block<MODE, E, O, KR, LPC>;
+  prep_smem((const void*)kern, gp.smem);
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, gp.block, gp.smem));
+  if (occ < 1) fail(FMV_EUNSUPPORTED, "block sbgemv: kernel does not fit on an SM");
+  long P = (long)sm_count(ctx->device) * std::min(occ, 2);
+  P = std::min(P, gp.p.T);
+  gp.p.P = (int)P;
+  if (MODE == GM_N) {
+    ctx->partials.ensure((size_t)(P + gp.p.batch) * KR * gp.p.m * sizeof(typename ET<E>::A));
+    gp.p.partials = ctx->partials.p;
+    gp.p.counters = ctx->tickets((size_t)gp.p.batch);
+  }
+  launch(ctx, MODE == GM_N ? 1 : 2, [&] { kern<<<(unsigned)P, gp.block, gp.smem, ctx->stream>>>(gp.p); });
+}
+
+template <int MODE, class E, class O>
+bool sbgemm_block_t(fmv_ctx* ctx, GemvPlan& gp) {
+  const int K = gp.p.K;
+  const int KR = K <= 2 ? 2 : K <= 4 ? 4 : 8;
+  if (!plan_block(gp, MODE, sizeof(E), sizeof(typename ET<E>::A), KR)) return false;
+  // ConjTrans lanes per column: 8 for columns up to 128 elements, else a warp
+  constexpr int L1 = MODE == GM_N ? 0 : 8, L2 = MODE == GM_N ? 0 : 32;
+  const bool wide = MODE != GM_N && gp.p.m > 128;
+  if (KR == 2) wide ? sbgemm_block_launch_t<MODE, E, O, 2, L2>(ctx, gp) : sbgemm_block_launch_t<MODE, E, O, 2, L1>(ctx, gp);
+  else if (KR == 4) wide ? sbgemm_block_launch_t<MODE, E, O, 4, L2>(ctx, gp) : sbgemm_block_launch_t<MODE, E, O, 4, L1>(ctx, gp);
+  else wide ? sbgemm_block_launch_t<MODE, E, O, 8, L2>(ctx, gp) : sbgemm_block_launch_t<MODE, E, O, 8, L1>(ctx, gp);
+  return true;
+}
+
+template <class E>
+bool sbgemm_block_e(fmv_ctx* ctx, int p3, int mode, GemvPlan& gp) {
+  if (mode == GM_N)
+    return p3 == PD ? sbgemm_block_t<GM_N, E, double2>(ctx, gp) : sbgemm_block_t<GM_N, E, float2>(ctx, gp);
+  return p3 == PD ? sbgemm_block_t<GM_C, E, double2>(ctx, gp) : sbgemm_block_t<GM_C, E, float2>(ctx, gp);
+}
+
+// Can the block kernel run this (op, cfg)? (fp16 'h' SBGEMV and NoTrans with
+// nd > 256 rows run as K single-RHS pipelines instead.)
+bool block_supported(const fmv_op* op, int kind, const std::array<int, 5>& p) {
+  if (p[2] == PH) return false;
+  return kind != FMV_FORWARD || op->nd <= (size_t)kConsumers;
+}
+
+// run_pipeline over K right-hand sides: in = K SOTI vectors back to back
+// (K*n_in*nt doubles), out likewise; device pointers, enqueued on ctx->stream.
+void pipeline_block(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5>& p, long K, const double* in,
+                    double* out) {
+  fmv_op* op = const_cast<fmv_op*>(cop);
+  const bool fwd = kind == FMV_FORWARD;
+  const long nt = (long)op->nt, nb = (long)op->nb();
+  const long n_in = fwd ? (long)op->nm : (long)op->nd;
+  const long n_out = fwd ? (long)op->nd : (long)op->nm;
+  if (K == 1 || !block_supported(op, kind, p)) {
+    for (long r = 0; r < K; ++r) pipeline(ctx, op, kind, p, in + r * n_in * nt, -1, out + r * n_out * nt);
+    return;
+  }
+  long lda = 0;
+  const void* bins = op_bins(ctx, op, p[2], &lda);
+  const size_t e2 = esize(p[2]), e3 = esize(p[3]);
+  const long sx = (n_in + 3) / 4 * 4;  // per-RHS spectrum stride in a bin (16-byte aligned)
+  ctx->x.ensure((size_t)nb * K * sx * e2 + 256);
+  ctx->y.ensure((size_t)nb * K * n_out * e3 + 256);
+  // phases 1-2: the K*n_in series in one launch when the RHS slices are contiguous
+  if (sx == n_in) {
+    r2c_dispatch<double>(ctx, p[0], p[1], p[2], in, nt, 1, K * n_in, (int)nt, (int)nt, ctx->x.p, K * sx, 1);
+  } else {
+    for (long r = 0; r < K; ++r)
+      r2c_dispatch<double>(ctx, p[0], p[1], p[2], in + r * n_in * nt, nt, 1, n_in, (int)nt, (int)nt,
+                           static_cast<unsigned char*>(ctx->x.p) + r * sx * e2, K * sx, 1);
+  }
+  // phase 3: block SBGEMV, <= kBlockMax RHS per launch
+  const long m = (long)op->nd, n = (long)op->nm;
+  const int kmax = block_max(fwd);
+  for (long r0 = 0; r0 < K; r0 += kmax) {
+    const int kc = (int)std::min<long>(kmax, K - r0);
+    GemvPlan gp = make_gemv(bins, m, n, nb, lda, n * lda, static_cast<unsigned char*>(ctx->x.p) + r0 * sx * e2, K * sx,
+                            static_cast<unsigned char*>(ctx->y.p) + r0 * n_out * e3, K * n_out);
+    gp.p.K = kc;
+    gp.p.sxr = sx;
+    gp.p.syr = n_out;
+    const int mode = fwd ? GM_N : GM_C;
+    const bool ok = p[2] == PD ? sbgemm_block_e<double2>(ctx, p[3], mode, gp) : sbgemm_block_e<float2>(ctx, p[3], mode, gp);
+    if (!ok) fail(FMV_EUNSUPPORTED, "block sbgemv: shape outside the staged kernel's limits");
+  }
+  // phases 4-5 over the K*n_out series
+  c2r_dispatch(ctx, p[3], p[4], ctx->y.p, K * n_out, 1, K * n_out, (int)nt, (int)nt, out, nt);
+  g_casts.fetch_add((uint64_t)K * count_casts(p, false), std::memory_order_relaxed);
+}
+
 // --------------------------------------------------------- cast kernels --
 template <class O>
 __global__ void k_cast_bins(const double2* __restrict__ in, O* __restrict__ out, long ncols, long nd, long lda_out) {
@@ -1187,6 +1324,42 @@ size_t fmv_op_device_bytes(const fmv_op* op) {
   return b;
 }
 
+int fmv_matvec_block_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, size_t nrhs, const double* d_in,
+                           double* d_out) {
+  return guarded([&] {
+    if (!ctx || !op || !d_in || !d_out) fail(FMV_EINVAL, "fmv_matvec_block_async: null argument");
+    if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
+    if (nrhs == 0) return;
+    const auto p = parse_cfg(cfg);
+    DeviceGuard dg(ctx->device);
+    pipeline_block(ctx, op, kind, p, (long)nrhs, d_in, d_out);
+  });
+}
+int fmv_matvec_block(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, size_t nrhs, const double* in,
+                     double* out, int io_on_device) {
+  return guarded([&] {
+    if (!ctx || !op || !in || !out) fail(FMV_EINVAL, "fmv_matvec_block: null argument");
+    if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
+    if (nrhs == 0) return;
+    const auto p = parse_cfg(cfg);
+    DeviceGuard dg(ctx->device);
+    const bool fwd = kind == FMV_FORWARD;
+    const size_t n_in = nrhs * (fwd ? op->nm : op->nd) * op->nt, n_out = nrhs * (fwd ? op->nd : op->nm) * op->nt;
+    const double* din = in;
+    double* dout = out;
+    cudaStream_t s = ctx->stream;
+    if (!io_on_device) {
+      ctx->io_in.ensure(n_in * sizeof(double));
+      ctx->io_out.ensure(n_out * sizeof(double));
+      din = static_cast<const double*>(ctx->io_in.p);
+      dout = static_cast<double*>(ctx->io_out.p);
+      CK(cudaMemcpyAsync(ctx->io_in.p, in, n_in * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    pipeline_block(ctx, op, kind, p, (long)nrhs, din, dout);
+    if (!io_on_device) CK(cudaMemcpyAsync(out, dout, n_out * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  });
+}
 int fmv_matvec_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* d_in, double* d_out) {
   return guarded([&] {
     if (!ctx || !op || !d_in || !d_out) fail(FMV_EINVAL, "fmv_matvec_async: null argument");

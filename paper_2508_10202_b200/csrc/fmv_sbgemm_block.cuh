@@ -1,0 +1,260 @@
+// fmv_sbgemm_block.cuh -- multi-RHS (block) SBGEMV for the block matvec
+// (Hessian assembly applies F / F* to many vectors,
+// PAPER.md:431-434, :510). Per frequency bin b the K right-hand sides are
+// handled together, so the operator -- the 8 GB that bounds a matvec -- is
+// streamed from HBM ONCE for all K:
+//   NoTrans (F):   Y_b[:, r] = A_b X_b[:, r]          (r < K)
+//   ConjTrans (F*): Z_b[:, r] = A_b^H D_b[:, r]
+// This is a complex GEMM with a skinny K (<= 8) and arithmetic intensity
+// 4K flop/B of operator (fp64): memory-bound up to K ~ 8 on B200's FP64 pipe,
+// so it stays on CUDA cores (tensor cores have no complex-fp64 advantage and
+// lower precision would change the result).
+//
+// Same producer / ring / flat-column-stream design as k_sbgemv (one
+// cp.async.bulk producer lane, nstage shared stages, equal pieces per
+// persistent CTA); one element per thread row (V = 1):
+//  * NoTrans: thread (r, g) owns row r, columns g, g+G, ... of each stage and
+//    keeps K accumulators; the stage's K x slices arrive with it. Bin flush
+//    and the cross-CTA (last-arriver, piece-ordered) reduction as k_sbgemv,
+//    with K*m partials per piece. fp32: per-stage partials folded with a
+//    Neumaier add, like the single-RHS kernel.
+//  * ConjTrans: LPC lanes per column split its rows (as k_sbgemv), each lane
+//    with K accumulators: A[i, c] is read once for all K right-hand sides,
+//    x_r[i] comes from the K vectors x_{b, r} kept resident per batch entry
+//    (two slots by batch parity); one xor-shuffle tree per RHS.
+#pragma once
+
+#include "fmv_sbgemv.cuh"
+
+namespace fmv {
+
+template <int MODE, class E, class O, int KR, int LPC>
+__global__ void __launch_bounds__(288, 2) k_sbgemm_block(const GemvParams p) {
+  using Tr = ET<E>;
+  using Acc = typename Tr::A;
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int ncons = blockDim.x - 32;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* empty = full + 16;
+  volatile int* s_flag = reinterpret_cast<volatile int*>(sm + 256);
+  unsigned char* stages = sm + 512;
+  const int xs_bytes = KR * p.xr_slot;  // all K x slices of one stage / batch entry
+  const int slot = p.a_slot + (p.xres ? 0 : xs_bytes);
+  unsigned char* xres_base = stages + (long)p.nstage * slot;
+  Acc* red = reinterpret_cast<Acc*>(xres_base + (p.xres ? 2L * xs_bytes : 0L));
+  const int K = p.K;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.nstage; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], ncons / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const long c0 = p.T * (long)blockIdx.x / p.P;
+  const long c1 = p.T * (long)(blockIdx.x + 1) / p.P;
+  constexpr int es = (int)sizeof(E);
+
+  if (threadIdx.x >= ncons) {
+    if (threadIdx.x != ncons) return;
+    const uint64_t pol_a = policy_evict_first();
+    const uint64_t pol_x = policy_evict_last();
+    long prev_b = -1;
+    for (SegIter sg(c0, c1, p); sg.more(); sg.advance(p)) {
+      sg.load(p);
+      const int s = sg.s;
+      mbar_wait(&empty[s], sg.par ^ 1u);
+      const bool new_x = !p.xres || sg.b != prev_b;
+      prev_b = sg.b;
+      const unsigned char* a0 = p.A + (sg.b * p.sa + sg.j * p.lda) * es;
+      const unsigned char* a_lo = reinterpret_cast<const unsigned char*>(reinterpret_cast<uintptr_t>(a0) & ~uintptr_t(15));
+      const uintptr_t a_end = reinterpret_cast<uintptr_t>(a0) + (uintptr_t)(((sg.cnt - 1) * p.lda + p.m) * es);
+      const uint32_t a_bytes = (uint32_t)(((a_end + 15) & ~uintptr_t(15)) - reinterpret_cast<uintptr_t>(a_lo));
+      const long xn = MODE == GM_N ? sg.cnt : p.m;
+      uint32_t xb[KR];
+      const unsigned char* xlo[KR];
+      uint32_t x_total = 0;
+#pragma unroll
+      for (int r = 0; r < KR; ++r) {
+        xb[r] = 0;
+        xlo[r] = nullptr;
+        if (r < K && new_x) {
+          const unsigned char* x0 = p.x + (sg.b * p.sx + r * p.sxr + (MODE == GM_N ? sg.j : 0)) * es;
+          xlo[r] = reinterpret_cast<const unsigned char*>(reinterpret_cast<uintptr_t>(x0) & ~uintptr_t(15));
+          const uintptr_t x_end = reinterpret_cast<uintptr_t>(x0) + (uintptr_t)(xn * es);
+          xb[r] = (uint32_t)(((x_end + 15) & ~uintptr_t(15)) - reinterpret_cast<uintptr_t>(xlo[r]));
+          x_total += xb[r];
+        }
+      }
+      unsigned char* dst = stages + (long)s * slot;
+      unsigned char* xdst = p.xres ? xres_base + (sg.b & 1) * (long)xs_bytes : dst + p.a_slot;
+      mbar_expect_tx(&full[s], a_bytes + x_total);
+      bulk_g2s(dst, a_lo, a_bytes, &full[s], pol_a);
+#pragma unroll
+      for (int r = 0; r < KR; ++r)
+        if (xb[r]) bulk_g2s(xdst + r * p.xr_slot, xlo[r], xb[r], &full[s], pol_x);
+    }
+    return;
+  }
+
+  const int t = threadIdx.x;
+  const int lane = t & 31;
+  if constexpr (MODE == GM_N) {
+    const int r = t % p.RT;
+    const int g = t / p.RT;
+    const bool active = g < p.G && r < p.m;
+    constexpr bool kComp = !std::is_same<Acc, double2>::value;
+    Acc acc[KR], cmp[KR];
+#pragma unroll
+    for (int k = 0; k < KR; ++k) acc[k] = cmp[k] = Tr::zero();
+    for (SegIter sg(c0, c1, p); sg.more(); sg.advance(p)) {
+      sg.load(p);
+      const int s = sg.s;
+      const unsigned char* a0 = p.A + (sg.b * p.sa + sg.j * p.lda) * es;
+      const unsigned char* base = stages + (long)s * slot;
+      const E* As = reinterpret_cast<const E*>(base + (reinterpret_cast<uintptr_t>(a0) & 15));
+      // x slice r starts at its slot + the source's offset within 16 bytes
+      const unsigned char* xbase = base + p.a_slot;
+      mbar_wait_sleep(&full[s], sg.par);
+      if (active) {
+        const int cnt = (int)sg.cnt;
+        Acc part[KR];
+#pragma unroll
+        for (int k = 0; k < KR; ++k) part[k] = kComp ? Tr::zero() : acc[k];
+        const E* Xs[KR];
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+          const unsigned char* x0 = p.x + (sg.b * p.sx + k * p.sxr + sg.j) * es;
+          Xs[k] = reinterpret_cast<const E*>(xbase + k * p.xr_slot + (reinterpret_cast<uintptr_t>(x0) & 15));
+        }
+        for (int jj = g; jj < cnt; jj += p.G) {
+          const E a = As[(long)jj * p.lda + r];
+#pragma unroll
+          for (int k = 0; k < KR; ++k)
+            if (k < K) part[k] = Tr::mac(part[k], a, Xs[k][jj]);
+        }
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+          if constexpr (kComp) neumaier_add(acc[k], cmp[k], part[k]);
+          else acc[k] = part[k];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (sg.ends_bin(p)) {
+        const int KM = K * p.m;
+        if (active) {
+#pragma unroll
+          for (int k = 0; k < KR; ++k) {
+            if (k < K) red[((long)g * K + k) * p.m + r] = kComp ? Tr::add(acc[k], cmp[k]) : acc[k];
+            acc[k] = cmp[k] = Tr::zero();
+          }
+        }
+        bar_consumers(ncons);
+        for (int i = t; i < KM; i += ncons) {
+          Acc v = red[i];
+          for (int gg = 1; gg < p.G; ++gg) v = Tr::add(v, red[(long)gg * KM + i]);
+          red[i] = v;
+        }
+        bar_consumers(ncons);
+        const long b = sg.b;
+        const long plo = piece_of(b * p.n, p.T, p.P);
+        const long phi = piece_of(b * p.n + p.n - 1, p.T, p.P);
+        O* yb = reinterpret_cast<O*>(p.y) + b * p.sy;
+        auto emit = [&](int i, Acc v) {
+          const int k = i / p.m, row = i - k * p.m;
+          yb[k * p.syr + row] = out_cast<O>(v);
+        };
+        if (plo == phi) {
+          for (int i = t; i < KM; i += ncons) emit(i, red[i]);
+        } else {
+          Acc* part = reinterpret_cast<Acc*>(p.partials);
+          const long slot_id = (long)blockIdx.x + b;
+          for (int i = t; i < KM; i += ncons) part[slot_id * KM + i] = red[i];
+          __threadfence();
+          bar_consumers(ncons);
+          if (t == 0) {
+            const unsigned prev = atomicAdd(&p.counters[b], 1u);
+            *s_flag = (prev == (unsigned)(phi - plo)) ? 1 : 0;
+          }
+          bar_consumers(ncons);
+          if (*s_flag) {
+            __threadfence();
+            for (int i = t; i < KM; i += ncons) {
+              Acc v = ldcg(part + (plo + b) * KM + i);
+              for (long pp = plo + 1; pp <= phi; ++pp) v = Tr::add(v, ldcg(part + (pp + b) * KM + i));
+              emit(i, v);
+            }
+            if (t == 0) p.counters[b] = 0u;
+          }
+        }
+        bar_consumers(ncons);
+      }
+    }
+  } else {
+    // LPC lanes per column split its m rows (lane li: rows li, li+LPC, ...);
+    // each lane keeps K accumulators, reads A[i, c] once for all K and
+    // x_r[i] from the resident slice (a broadcast across the warp's columns);
+    // then one xor-shuffle tree per RHS and lane li stores RHS li (and
+    // li + LPC, ...).
+    constexpr int CPW = 32 / LPC;
+    const int W = ncons / 32;
+    const int w = t >> 5;
+    const int sub = lane / LPC;
+    const int li = lane - sub * LPC;
+    for (SegIter sg(c0, c1, p); sg.more(); sg.advance(p)) {
+      sg.load(p);
+      const int s = sg.s;
+      const unsigned char* a0 = p.A + (sg.b * p.sa + sg.j * p.lda) * es;
+      const unsigned char* base = stages + (long)s * slot;
+      const E* As = reinterpret_cast<const E*>(base + (reinterpret_cast<uintptr_t>(a0) & 15));
+      const unsigned char* xb = p.xres ? xres_base + (sg.b & 1) * (long)xs_bytes : base + p.a_slot;
+      const E* Xs[KR];
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        const int kk = min(k, K - 1);
+        const unsigned char* x0 = p.x + (sg.b * p.sx + (long)kk * p.sxr) * es;
+        Xs[k] = reinterpret_cast<const E*>(xb + kk * p.xr_slot + (reinterpret_cast<uintptr_t>(x0) & 15));
+      }
+      O* yb = reinterpret_cast<O*>(p.y) + sg.b * p.sy + sg.j;
+      mbar_wait_sleep(&full[s], sg.par);
+      const int cnt = (int)sg.cnt;
+      for (int jb = w * CPW; jb < cnt; jb += W * CPW) {
+        const int jj = jb + sub;
+        const bool valid = jj < cnt;
+        Acc acc[KR];
+#pragma unroll
+        for (int k = 0; k < KR; ++k) acc[k] = Tr::zero();
+        if (valid) {
+          const E* col = As + (long)jj * p.lda;
+          for (int i = li; i < p.m; i += LPC) {
+            const E a = col[i];
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+              if (k < K) {
+                if constexpr (MODE == GM_C) acc[k] = Tr::macc(acc[k], a, Xs[k][i]);
+                else acc[k] = Tr::mac(acc[k], a, Xs[k][i]);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+#pragma unroll
+          for (int o = LPC >> 1; o > 0; o >>= 1) acc[k] = Tr::add(acc[k], Tr::shfl_xor(acc[k], o));
+        }
+        if (valid) {
+#pragma unroll
+          for (int k = 0; k < KR; ++k)
+            if (k < K && k % LPC == li) yb[(long)k * p.syr + jj] = out_cast<O>(acc[k]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
+}
+
+}  // namespace fmv

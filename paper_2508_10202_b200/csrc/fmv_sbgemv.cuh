@@ -263,6 +263,12 @@ struct GemvParams {
   int xres;
   int xres_slot;
   int arrive_all;  // every consumer thread arrives on the empty barrier (else one lane per warp)
+  // Block (multi-RHS) kernel k_sbgemm_block only: K right-hand sides per
+  // batch entry, x_{b,r} at x + (b*sx + r*sxr)*es and y_{b,r} at
+  // y + (b*sy + r*syr)*es; xr_slot = shared bytes per RHS x slice.
+  int K;
+  long sxr, syr;
+  int xr_slot;
 };
 
 __device__ __forceinline__ long piece_of(long c, long T, int P) {

@@ -33,6 +33,7 @@ __all__ = [
     "setup_operator", "materialize_single", "MatvecKind", "PhaseTimings", "MatvecResult", "phase_name",
     "forward_matvec", "adjoint_matvec", "run_pipeline", "Context", "default_context", "casts_performed",
     "reset_cast_counter", "uniform_fill", "seed_stream", "non_representable_fill", "relative_error", "FmvError",
+    "matvec_block", "forward_matvec_block", "adjoint_matvec_block",
 ]
 
 
@@ -454,6 +455,47 @@ def adjoint_matvec(op: SpectralOperator, d: BlockVector, cfg="ddddd", tiling=Non
     _check_input(op, d, False)
     out, t = run_pipeline(op, MatvecKind.Adjoint, d.data, cfg)
     return MatvecResult(BlockVector.time_double(op.dims.n_m, op.dims.n_t, out), t)
+
+
+def matvec_block(op: SpectralOperator, kind: MatvecKind, inp, cfg="ddddd", ctx: Optional[Context] = None):
+    """Block (multi-RHS) matvec: applies F (Forward) or F*
+    (Adjoint) to K vectors at once. ``inp`` is (K, n_in*nt) float64 -- a
+    numpy array (host I/O) or a CUDA torch tensor (device I/O); returns
+    (K, n_out*nt) of the same kind. Row r equals run_pipeline(op, kind,
+    inp[r], cfg) up to summation order; the operator is streamed from HBM
+    once per 8 right-hand sides."""
+    ctx = ctx or op.ctx
+    fwd = kind == MatvecKind.Forward
+    n_in = (op.dims.n_m if fwd else op.dims.n_d) * op.dims.n_t
+    n_out = (op.dims.n_d if fwd else op.dims.n_m) * op.dims.n_t
+    cs = _cfg_str(cfg).encode()
+    if _is_cuda_tensor(inp):
+        import torch
+
+        if inp.dtype != torch.float64 or inp.dim() != 2 or inp.shape[1] != n_in:
+            raise ValueError("matvec_block: input must be (K, n_in*n_t) float64")
+        x = inp.contiguous()
+        out = torch.empty((x.shape[0], n_out), dtype=torch.float64, device=x.device)
+        torch.cuda.current_stream(x.device).synchronize()
+        check(lib().fmv_matvec_block(ctx.handle, op.handle, int(kind), cs, x.shape[0], ctypes.c_void_p(x.data_ptr()),
+                                     ctypes.c_void_p(out.data_ptr()), 1))
+        return out
+    x = np.ascontiguousarray(inp, dtype=np.float64)
+    if x.ndim != 2 or x.shape[1] != n_in:
+        raise ValueError("matvec_block: input must be (K, n_in*n_t) float64")
+    out = np.empty((x.shape[0], n_out), dtype=np.float64)
+    check(lib().fmv_matvec_block(ctx.handle, op.handle, int(kind), cs, x.shape[0], x.ctypes.data, out.ctypes.data, 0))
+    return out
+
+
+def forward_matvec_block(op: SpectralOperator, M, cfg="ddddd"):
+    """D = F M for K parameter vectors (rows of M, each n_m*n_t, SOTI)."""
+    return matvec_block(op, MatvecKind.Forward, M, cfg)
+
+
+def adjoint_matvec_block(op: SpectralOperator, D, cfg="ddddd"):
+    """M = F* D for K sensor vectors (rows of D, each n_d*n_t, SOTI)."""
+    return matvec_block(op, MatvecKind.Adjoint, D, cfg)
 
 
 def casts_performed() -> int:

@@ -123,6 +123,21 @@ static void gpu_checks() {
     EXPECT(relative_error(pf.output.f64, F.output.f64) <= 1e-12);
     EXPECT(relative_error(pa.output.f64, A.output.f64) <= 1e-12);
   }
+  // block (multi-RHS) matvecs: every RHS equals the single-RHS result to rounding
+  {
+    std::vector<BlockVector> ms, ds;
+    for (int r = 0; r < 3; ++r) {
+      ms.push_back(BlockVector::time_double(dims.n_m, dims.n_t, uniform_fill(dims.n_m * dims.n_t, 40 + r)));
+      ds.push_back(BlockVector::time_double(dims.n_d, dims.n_t, uniform_fill(dims.n_d * dims.n_t, 50 + r)));
+    }
+    auto BF = forward_matvec_block(op, ms);
+    auto BA = adjoint_matvec_block(op, ds);
+    EXPECT(BF.size() == 3 && BA.size() == 3);
+    for (int r = 0; r < 3; ++r) {
+      EXPECT(relative_error(BF[r].f64, forward_matvec(op, ms[r], PrecisionConfig{}).output.f64) <= 1e-14);
+      EXPECT(relative_error(BA[r].f64, adjoint_matvec(op, ds[r], PrecisionConfig{}).output.f64) <= 1e-14);
+    }
+  }
   // FFT facade round trip
   FftPlan fwd(16, 3, Precision::Double, FftDirection::Forward), inv(16, 3, Precision::Double, FftDirection::Inverse);
   auto x = uniform_fill(48, 3);
