@@ -145,6 +145,22 @@ int fmv_comm_destroy(fmv_ctx* ctx);
 int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* shard, int kind, const char* cfg, const double* in,
                            double* out, int io_on_device, fmv_phase_times* times);
 
+/* ---- 2-D pr x pc grid ----
+ * rank = ri*pc + cj. Splits the world communicator into a row communicator
+ * (the pc ranks of grid row ri) and a column communicator (the pr ranks of
+ * grid column cj) with ncclCommSplit. */
+int fmv_comm_init_2d(fmv_ctx* ctx, int pr, int pc, int rank, const void* id128);
+/* Each rank holds the (ri, cj) operator block: sensor rows of grid row ri x
+ * parameter columns of grid column cj (GridPxQ, partition.py).
+ * FORWARD: in = m_cj (read on grid row 0 only), rounded to cfg[0] and
+ *   broadcast down the column; partial d_ri summed along the row in cfg[4];
+ *   out = d_ri (nd_ri*nt) on every rank of the row.
+ * ADJOINT: in = d_ri (read on grid column 0 only), rounded to cfg[0] and
+ *   broadcast along the row; partial m_cj summed down the column in cfg[4];
+ *   out = m_cj (nm_cj*nt) on every rank of the column. */
+int fmv_matvec_partitioned_2d(fmv_ctx* ctx, const fmv_op* shard, int kind, const char* cfg, const double* in,
+                              double* out, int io_on_device);
+
 /* ---- host helpers kept from the reference API ---- */
 uint64_t fmv_seed_stream(uint64_t seed, uint64_t stream);                          /* random_fill.hpp:30-32 */
 void fmv_uniform_fill(size_t count, uint64_t seed, double lo, double hi, double* out); /* random_fill.hpp:17-27 */

@@ -266,6 +266,7 @@ struct Nccl {
   typedef int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t);
   typedef int (*Broadcast)(const void*, void*, size_t, int, int, void*, cudaStream_t);
   typedef int (*CommDestroy)(void*);
+  typedef int (*CommSplit)(void*, int, int, void**, void*);
   typedef const char* (*GetErrorString)(int);
   void* h = nullptr;
   GetUniqueId get_unique_id = nullptr;
@@ -273,6 +274,7 @@ struct Nccl {
   AllReduce all_reduce = nullptr;
   Broadcast broadcast = nullptr;
   CommDestroy comm_destroy = nullptr;
+  CommSplit comm_split = nullptr;
   GetErrorString err = nullptr;
 };
 Nccl& nccl() {
@@ -288,6 +290,7 @@ Nccl& nccl() {
     n.all_reduce = (Nccl::AllReduce)dlsym(n.h, "ncclAllReduce");
     n.broadcast = (Nccl::Broadcast)dlsym(n.h, "ncclBroadcast");
     n.comm_destroy = (Nccl::CommDestroy)dlsym(n.h, "ncclCommDestroy");
+    n.comm_split = (Nccl::CommSplit)dlsym(n.h, "ncclCommSplit");
     n.err = (Nccl::GetErrorString)dlsym(n.h, "ncclGetErrorString");
   });
   if (!n.h || !n.get_unique_id || !n.comm_init_rank || !n.all_reduce || !n.broadcast)
@@ -344,6 +347,11 @@ struct fmv_ctx {
   uint64_t prof_n[5] = {0, 0, 0, 0, 0};
   void* comm = nullptr;
   int nranks = 1, rank = 0;
+  // 2-D pr x pc grid (fmv_comm_init_2d): rank = ri * pc + cj; row_comm joins
+  // the pc ranks of grid row ri, col_comm the pr ranks of grid column cj.
+  void* row_comm = nullptr;
+  void* col_comm = nullptr;
+  int pr = 1, pc = 1, ri = 0, cj = 0;
   cudaEvent_t te[8] = {};
 
   cudaEvent_t ev() {
@@ -1136,6 +1144,50 @@ const void* op_bins(fmv_ctx* ctx, fmv_op* op, int prec, long* lda) {
 // ======================================================================
 // C ABI
 // ======================================================================
+namespace {
+// Round `in` (n doubles, valid on the group root) to cfg[0] precision once and
+// broadcast it over `comm` (group size gsize): the payload semantics of
+// partition.hpp:196-206. Returns the payload pointer and its precision.
+std::pair<const void*, int> bcast_payload(fmv_ctx* ctx, void* comm, int gsize, bool root, const double* in, long n,
+                                          int p0) {
+  cudaStream_t s = ctx->stream;
+  if (p0 == PD) {
+    if (gsize == 1) return {in, PD};
+    ctx->payload.ensure(n * sizeof(double));
+    if (root) CK(cudaMemcpyAsync(ctx->payload.p, in, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    nck(nccl().broadcast(ctx->payload.p, ctx->payload.p, n, kNcclDouble, 0, comm, s), "ncclBroadcast");
+    return {ctx->payload.p, PD};
+  }
+  ctx->payload.ensure(n * sizeof(float));
+  if (root) {
+    if (p0 == PS)
+      launch(ctx, 4, [&] { k_d2f<<<grid_for(n, 256, ctx->device), 256, 0, s>>>(in, static_cast<float*>(ctx->payload.p), n); });
+    else
+      launch(ctx, 4, [&] { k_d2h<<<grid_for(n, 256, ctx->device), 256, 0, s>>>(in, static_cast<__half*>(ctx->payload.p), n); });
+    g_casts.fetch_add(1, std::memory_order_relaxed);  // partition.hpp:203
+  }
+  if (gsize > 1)
+    nck(nccl().broadcast(ctx->payload.p, ctx->payload.p, n, p0 == PS ? kNcclFloat : kNcclHalf, 0, comm, s),
+        "ncclBroadcast");
+  return {ctx->payload.p, p0};
+}
+
+// Sum the n-double partial `buf` over `comm` in cfg[4] precision (partition.hpp:175-177).
+void allreduce_prec(fmv_ctx* ctx, void* comm, int gsize, double* buf, long n, int p4) {
+  if (gsize == 1) return;
+  cudaStream_t s = ctx->stream;
+  if (p4 == PD) {
+    nck(nccl().all_reduce(buf, buf, n, kNcclDouble, kNcclSum, comm, s), "ncclAllReduce");
+    return;
+  }
+  ctx->red.ensure(n * sizeof(float));
+  float* f = static_cast<float*>(ctx->red.p);
+  launch(ctx, 4, [&] { k_d2f<<<grid_for(n, 256, ctx->device), 256, 0, s>>>(buf, f, n); });
+  nck(nccl().all_reduce(f, f, n, kNcclFloat, kNcclSum, comm, s), "ncclAllReduce");
+  launch(ctx, 4, [&] { k_f2d<<<grid_for(n, 256, ctx->device), 256, 0, s>>>(f, buf, n); });
+}
+}  // namespace
+
 extern "C" {
 
 const char* fmv_last_error(void) { return g_err.c_str(); }
@@ -1514,10 +1566,31 @@ int fmv_comm_init(fmv_ctx* ctx, int nranks, int rank, const void* id128) {
 int fmv_comm_destroy(fmv_ctx* ctx) {
   return guarded([&] {
     if (!ctx) fail(FMV_EINVAL, "null ctx");
-    if (ctx->comm && nccl().comm_destroy) nccl().comm_destroy(ctx->comm);
-    ctx->comm = nullptr;
+    for (void** c : {&ctx->row_comm, &ctx->col_comm, &ctx->comm}) {
+      if (*c && nccl().comm_destroy) nccl().comm_destroy(*c);
+      *c = nullptr;
+    }
     ctx->nranks = 1;
     ctx->rank = 0;
+    ctx->pr = ctx->pc = 1;
+    ctx->ri = ctx->cj = 0;
+  });
+}
+
+int fmv_comm_init_2d(fmv_ctx* ctx, int pr, int pc, int rank, const void* id128) {
+  return guarded([&] {
+    if (!ctx || pr < 1 || pc < 1 || rank < 0 || rank >= pr * pc) fail(FMV_EINVAL, "fmv_comm_init_2d: bad arguments");
+    const int rc = fmv_comm_init(ctx, pr * pc, rank, id128);
+    if (rc != FMV_OK) fail(rc, fmv_last_error());
+    DeviceGuard dg(ctx->device);
+    ctx->pr = pr;
+    ctx->pc = pc;
+    ctx->ri = rank / pc;
+    ctx->cj = rank % pc;
+    if (pr * pc == 1) return;
+    if (!nccl().comm_split) fail(FMV_ENCCL, "ncclCommSplit is not available in the loaded NCCL");
+    nck(nccl().comm_split(ctx->comm, ctx->ri, ctx->cj, &ctx->row_comm, nullptr), "ncclCommSplit(row)");
+    nck(nccl().comm_split(ctx->comm, ctx->cj, ctx->ri, &ctx->col_comm, nullptr), "ncclCommSplit(col)");
   });
 }
 
@@ -1621,6 +1694,50 @@ int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* op, int kind, const char*
       }
       times->total_s = (a + b + c + d) * 1e-3;
     }
+  });
+}
+
+// 2-D pr x pc grid: grid row ri owns sensor
+// rows [dlo, dhi), grid column cj owns parameter columns [mlo, mhi); this
+// rank's shard is the (ri, cj) sub-block of every time block.
+// FORWARD: in = m_cj (nm_cj*nt), read on grid row 0 only; it is rounded to
+//   cfg[0] and broadcast down the column, each rank computes its partial
+//   d_ri, and the row all-reduces it in cfg[4]: out = d_ri (nd_ri*nt) on
+//   every rank of grid row ri.
+// ADJOINT: in = d_ri (nd_ri*nt), read on grid column 0 only; rounded to
+//   cfg[0] and broadcast along the row, partial m_cj all-reduced down the
+//   column in cfg[4]: out = m_cj (nm_cj*nt) on every rank of grid column cj.
+// With pr = 1 this is the 1 x p partition (the forward input is then local).
+int fmv_matvec_partitioned_2d(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* in,
+                              double* out, int io_on_device) {
+  return guarded([&] {
+    if (!ctx || !op || !out) fail(FMV_EINVAL, "fmv_matvec_partitioned_2d: null argument");
+    if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
+    const auto p = parse_cfg(cfg);
+    DeviceGuard dg(ctx->device);
+    cudaStream_t s = ctx->stream;
+    const bool fwd = kind == FMV_FORWARD;
+    const size_t nt = op->nt;
+    const size_t n_in = (fwd ? op->nm : op->nd) * nt, n_out = (fwd ? op->nd : op->nm) * nt;
+    const bool root = fwd ? ctx->ri == 0 : ctx->cj == 0;
+    void* bcomm = fwd ? ctx->col_comm : ctx->row_comm;
+    void* rcomm = fwd ? ctx->row_comm : ctx->col_comm;
+    const int bsize = fwd ? ctx->pr : ctx->pc, rsize = fwd ? ctx->pc : ctx->pr;
+    if (root && !in) fail(FMV_EINVAL, "fmv_matvec_partitioned_2d: null input on a root rank");
+    const double* din = in;
+    double* dout = out;
+    if (!io_on_device) {
+      ctx->io_in.ensure(n_in * sizeof(double));
+      ctx->io_out.ensure(n_out * sizeof(double));
+      if (root) CK(cudaMemcpyAsync(ctx->io_in.p, in, n_in * sizeof(double), cudaMemcpyHostToDevice, s));
+      din = static_cast<const double*>(ctx->io_in.p);
+      dout = static_cast<double*>(ctx->io_out.p);
+    }
+    const auto pay = bcast_payload(ctx, bcomm, bsize, root, din, (long)n_in, p[0]);
+    pipeline(ctx, op, kind, p, pay.first, pay.second, dout);
+    allreduce_prec(ctx, rcomm, rsize, dout, (long)n_out, p[4]);
+    if (!io_on_device) CK(cudaMemcpyAsync(out, dout, n_out * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
   });
 }
 

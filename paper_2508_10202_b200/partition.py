@@ -31,7 +31,8 @@ from .fftmv import (BlockColumn, BlockVector, Context, Domain, Layout, MatvecKin
 
 __all__ = ["Grid1xP", "CommSpec", "shard_operator", "tree_reduce", "PartitionedOperator", "PartitionedResult",
            "setup_partitioned", "forward_matvec_partitioned", "adjoint_matvec_partitioned", "round_to",
-           "DistributedMatvec"]
+           "DistributedMatvec", "GridPxQ", "shard_operator_2d", "PartitionedOperator2D", "setup_partitioned_2d",
+           "forward_matvec_partitioned_2d", "adjoint_matvec_partitioned_2d", "DistributedMatvec2D"]
 
 
 @dataclass
@@ -281,6 +282,216 @@ class DistributedMatvec:
                                                ctypes.byref(t)))
         if times:
             return out, PhaseTimings(list(t.phase_s), t.total_s)
+        return out
+
+    def close(self):
+        if self.transport == "native" and self.ctx is not None:
+            lib().fmv_comm_destroy(self.ctx.handle)
+
+
+# ================================================================ 2-D grid ===
+# SURVEY.md §8 f3 / PAPER.md:341: the 1D column partition generalised to a
+# pr x pc grid that splits the sensor rows (Nd) as well as the parameter
+# columns (Nm). Rank r sits at grid position (ri, cj) = divmod(r, pc) and
+# holds block (ri, cj) of every time block. F: m_cj is broadcast down grid
+# column cj (in cfg[0], the pad precision: the payload semantics of the 1 x p
+# adjoint, partition.hpp:196-206), every rank computes its partial d_ri, and
+# the pc partials of grid row ri are summed in cfg[4] (partition.hpp:175-177).
+# F* is the mirror image: d_ri broadcast along the row, partial m_cj summed
+# down the column. pr = 1 is exactly the 1 x p partition.
+
+
+def _balanced(p: int, n: int, what: str) -> List[tuple]:
+    if p < 1:
+        raise ValueError(f"GridPxQ: {what} must be >= 1")
+    if p > n:
+        raise ValueError(f"GridPxQ: more {what} than extent {n}")
+    base, rem = divmod(n, p)
+    out, b = [], 0
+    for w in range(p):
+        sz = base + (1 if w < rem else 0)
+        out.append((b, b + sz))
+        b += sz
+    return out
+
+
+@dataclass
+class GridPxQ:
+    """pr x pc grid: row ranges over Nd, column ranges over Nm (both split
+    like Grid1xP::split, partition.hpp:27-40); rank = ri * pc + cj."""
+
+    pr: int = 1
+    pc: int = 1
+    row_ranges: List[tuple] = field(default_factory=list)
+    col_ranges: List[tuple] = field(default_factory=list)
+
+    @staticmethod
+    def split(pr: int, pc: int, n_d: int, n_m: int) -> "GridPxQ":
+        return GridPxQ(pr, pc, _balanced(pr, n_d, "grid rows"), _balanced(pc, n_m, "grid columns"))
+
+    @property
+    def size(self) -> int:
+        return self.pr * self.pc
+
+    def coords(self, rank: int) -> tuple:
+        if not 0 <= rank < self.size:
+            raise ValueError("GridPxQ: rank out of range")
+        return divmod(rank, self.pc)
+
+
+def shard_operator_2d(col: BlockColumn, grid: GridPxQ) -> List[BlockColumn]:
+    """Block (ri, cj) of every time block, in rank order (ri * pc + cj)."""
+    d = col.dims
+    if grid.row_ranges[-1][1] != d.n_d or grid.col_ranges[-1][1] != d.n_m:
+        raise ValueError("shard_operator_2d: grid does not cover (n_d, n_m)")
+    blocks = np.asarray(col.data).reshape(d.n_t, d.n_m, d.n_d)  # [t][j][i]
+    out = []
+    for dlo, dhi in grid.row_ranges:
+        for mlo, mhi in grid.col_ranges:
+            sub = np.ascontiguousarray(blocks[:, mlo:mhi, dlo:dhi]).reshape(-1)
+            out.append(BlockColumn(ProblemDims(mhi - mlo, dhi - dlo, d.n_t), sub))
+    return out
+
+
+@dataclass
+class PartitionedOperator2D:
+    dims: ProblemDims
+    grid: GridPxQ
+    workers: List[SpectralOperator]  # rank order
+
+
+def setup_partitioned_2d(col: BlockColumn, grid: GridPxQ, ctx: Optional[Context] = None) -> PartitionedOperator2D:
+    return PartitionedOperator2D(col.dims, grid, [setup_operator(s, ctx) for s in shard_operator_2d(col, grid)])
+
+
+def _matvec_2d(pop: PartitionedOperator2D, x, cfg, fwd: bool, compute=None) -> PartitionedResult:
+    c = _cfg_str(cfg)
+    nt = pop.dims.n_t
+    g = pop.grid
+    x = np.ascontiguousarray(x.data if isinstance(x, BlockVector) else x, dtype=np.float64).reshape(-1)
+    if x.size != (pop.dims.n_m if fwd else pop.dims.n_d) * nt:
+        raise ValueError("partitioned matvec: input extents do not match dims")
+    kind = MatvecKind.Forward if fwd else MatvecKind.Adjoint
+    run = compute or (lambda r, k, cc, v: run_pipeline(pop.workers[r], k, v, cc)[0])
+    in_ranges, out_ranges = (g.col_ranges, g.row_ranges) if fwd else (g.row_ranges, g.col_ranges)
+    payloads = [round_to(x[lo * nt:hi * nt], c[0]) for lo, hi in in_ranges]  # broadcast once per input slice
+    out = np.empty((pop.dims.n_d if fwd else pop.dims.n_m) * nt)
+    for o, (lo, hi) in enumerate(out_ranges):
+        partials = []
+        for i in range(len(in_ranges)):
+            r = o * g.pc + i if fwd else i * g.pc + o
+            partials.append(np.asarray(run(r, kind, _payload_cfg(c), payloads[i])))
+        out[lo * nt:hi * nt] = tree_reduce(partials, Precision.Double if c[4] == "d" else Precision.Single) \
+            if len(partials) > 1 else partials[0]
+    return PartitionedResult(BlockVector.time_double(pop.dims.n_d if fwd else pop.dims.n_m, nt, out), PhaseTimings())
+
+
+def forward_matvec_partitioned_2d(pop: PartitionedOperator2D, m, cfg="ddddd") -> PartitionedResult:
+    """d = F m on the pr x pc grid, simulated in process (one GPU, shards in
+    rank order, row sums in the fixed tree_reduce order)."""
+    return _matvec_2d(pop, m, cfg, True)
+
+
+def adjoint_matvec_partitioned_2d(pop: PartitionedOperator2D, d, cfg="ddddd") -> PartitionedResult:
+    """m = F* d on the pr x pc grid, simulated in process."""
+    return _matvec_2d(pop, d, cfg, False)
+
+
+class DistributedMatvec2D:
+    """One rank of a pr x pc grid (rank = ri * pc + cj).
+
+    transport="native": NCCL row/column communicators inside libfftmv_cuda
+      (fmv_comm_init_2d, ncclCommSplit) and fmv_matvec_partitioned_2d.
+    transport="torch": torch.distributed row/column groups (gloo or nccl) on
+      host arrays with an injectable ``compute(kind, cfg, x)`` -- the CPU
+      tests of the orchestration.
+    forward(m_cj) -> d_ri (m_cj needed on grid row 0 only); adjoint(d_ri) ->
+    m_cj (d_ri needed on grid column 0 only).
+    """
+
+    def __init__(self, dims: ProblemDims, pr: int, pc: int, rank: int, shard: Optional[SpectralOperator] = None,
+                 transport: str = "native", compute: Optional[Callable] = None, ctx: Optional[Context] = None):
+        self.dims = dims
+        self.grid = GridPxQ.split(pr, pc, dims.n_d, dims.n_m)
+        self.rank = rank
+        self.ri, self.cj = self.grid.coords(rank)
+        self.dlo, self.dhi = self.grid.row_ranges[self.ri]
+        self.mlo, self.mhi = self.grid.col_ranges[self.cj]
+        self.shard = shard
+        self.transport = transport
+        self.ctx = ctx or (shard.ctx if shard is not None else None)
+        if transport == "native":
+            if shard is None:
+                raise ValueError("native transport needs the rank's SpectralOperator shard")
+            import torch.distributed as dist
+
+            idb = (ctypes.c_char * 128)()
+            if self.grid.size > 1:
+                if rank == 0:
+                    check(lib().fmv_comm_unique_id(idb))
+                obj = [bytes(idb)] if rank == 0 else [None]
+                dist.broadcast_object_list(obj, src=0)
+                idb = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+            check(lib().fmv_comm_init_2d(self.ctx.handle, pr, pc, rank, idb))
+        elif transport == "torch":
+            import torch.distributed as dist
+
+            self.compute = compute or (lambda kind, cfg, x: run_pipeline(self.shard, kind, x, cfg)[0])
+            # every rank creates every group in the same order (torch.distributed requirement)
+            self.rows = [dist.new_group([i * pc + j for j in range(pc)]) if pr * pc > 1 else None for i in range(pr)]
+            self.cols = [dist.new_group([i * pc + j for i in range(pr)]) if pr * pc > 1 else None for j in range(pc)]
+        else:
+            raise ValueError("transport must be 'native' or 'torch'")
+
+    def _torch(self, kind, c, x, bgroup, broot, bsize, rgroup, rsize, n_in):
+        import torch
+        import torch.distributed as dist
+
+        bdt = {"d": np.float64, "s": np.float32, "h": np.float16}[c[0]]
+        buf = np.zeros(n_in, dtype=bdt)
+        if x is not None:
+            buf[:] = np.asarray(x, dtype=np.float64).astype(bdt)
+        t = torch.from_numpy(buf)
+        if bsize > 1:
+            dist.broadcast(t, src=broot, group=bgroup)
+        part = np.asarray(self.compute(kind, _payload_cfg(c), t.numpy().astype(np.float64)))
+        if rsize == 1:
+            return part
+        r = torch.from_numpy(part.astype(np.float64 if c[4] == "d" else np.float32))
+        dist.all_reduce(r, op=dist.ReduceOp.SUM, group=rgroup)
+        return r.numpy().astype(np.float64)
+
+    def forward(self, m_slice, cfg="ddddd"):
+        c = _cfg_str(cfg)
+        nt = self.dims.n_t
+        g = self.grid
+        if self.transport == "native":
+            return self._native(MatvecKind.Forward, c, m_slice, (self.dhi - self.dlo) * nt)
+        return self._torch(MatvecKind.Forward, c, m_slice if self.ri == 0 else None, self.cols[self.cj], self.cj, g.pr,
+                           self.rows[self.ri], g.pc, (self.mhi - self.mlo) * nt)
+
+    def adjoint(self, d_slice, cfg="ddddd"):
+        c = _cfg_str(cfg)
+        nt = self.dims.n_t
+        g = self.grid
+        if self.transport == "native":
+            return self._native(MatvecKind.Adjoint, c, d_slice, (self.mhi - self.mlo) * nt)
+        return self._torch(MatvecKind.Adjoint, c, d_slice if self.cj == 0 else None, self.rows[self.ri],
+                           self.ri * g.pc, g.pc, self.cols[self.cj], g.pr, (self.dhi - self.dlo) * nt)
+
+    def _native(self, kind, c, x, n_out):
+        if _is_cuda_tensor(x):
+            import torch
+
+            out = torch.empty(n_out, dtype=torch.float64, device=x.device)
+            torch.cuda.current_stream(x.device).synchronize()
+            check(lib().fmv_matvec_partitioned_2d(self.ctx.handle, self.shard.handle, int(kind), c.encode(),
+                                                  ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), 1))
+            return out
+        out = np.empty(n_out)
+        xin = None if x is None else np.ascontiguousarray(x, dtype=np.float64)
+        check(lib().fmv_matvec_partitioned_2d(self.ctx.handle, self.shard.handle, int(kind), c.encode(),
+                                              None if xin is None else xin.ctypes.data, out.ctypes.data, 0))
         return out
 
     def close(self):

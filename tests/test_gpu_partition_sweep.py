@@ -50,6 +50,45 @@ def test_native_partition_entry_world1_is_bitwise_serial():
     dm.close()
 
 
+def test_grid2d_in_process_vs_serial_and_1xp():
+    """pr x pc grid simulated on one GPU. ddddd within 1e-12
+    of the serial matvec for every grid; pr = 1 is the 1 x p partition
+    bitwise; mixed configs within the serial config's error scale."""
+    nm, nd, nt = 60, 9, 100
+    col, m, d = make_inputs(F, nm, nd, nt)
+    dims = F.ProblemDims(nm, nd, nt)
+    serial = F.setup_operator(F.BlockColumn(dims, col))
+    sf, sa = F.forward_matvec(serial, m).output.data, F.adjoint_matvec(serial, d).output.data
+    for pr, pc in ((1, 1), (1, 3), (2, 1), (2, 2), (3, 4)):
+        pop = F.setup_partitioned_2d(F.BlockColumn(dims, col), F.GridPxQ.split(pr, pc, nd, nm))
+        for cfg in ("ddddd", "dssdd", "sddds"):
+            pf = F.forward_matvec_partitioned_2d(pop, m, cfg).output.data
+            pa = F.adjoint_matvec_partitioned_2d(pop, d, cfg).output.data
+            if cfg == "ddddd":
+                assert rel(pf, sf) <= 1e-12 and rel(pa, sa) <= 1e-12, (pr, pc)
+            else:
+                ef = rel(F.forward_matvec(serial, m, cfg).output.data, sf)
+                ea = rel(F.adjoint_matvec(serial, d, cfg).output.data, sa)
+                assert rel(pf, sf) <= 4 * ef + 1e-12 and rel(pa, sa) <= 4 * ea + 1e-12, (pr, pc, cfg)
+            if pr == 1:
+                q = F.setup_partitioned(F.BlockColumn(dims, col), F.Grid1xP.split(pc, nm))
+                assert np.array_equal(pf, F.forward_matvec_partitioned(q, m, cfg).output.data), (pc, cfg)
+                assert np.array_equal(pa, F.adjoint_matvec_partitioned(q, d, cfg).output.data), (pc, cfg)
+
+
+def test_native_grid2d_entry_world1_is_bitwise_serial():
+    nm, nd, nt = 40, 6, 30
+    col, m, d = make_inputs(F, nm, nd, nt)
+    dims = F.ProblemDims(nm, nd, nt)
+    op = F.setup_operator(F.BlockColumn(dims, col))
+    dm = F.DistributedMatvec2D(dims, 1, 1, 0, shard=op, transport="native")
+    for cfg in ("ddddd", "dssds", "sdddd", "hdhdh"):
+        assert np.array_equal(dm.forward(m, cfg), F.forward_matvec(op, m, cfg).output.data), cfg
+        want = F.adjoint_matvec(op, F.round_to(d, cfg[0]), "d" + cfg[1:]).output.data
+        assert np.array_equal(dm.adjoint(d, cfg), want), cfg
+    dm.close()
+
+
 def test_sweep_acceptance5_and_pareto():
     """SPEC.md:544 at 500/20/200, non-representable fill, 32 rows."""
     nm, nd, nt = 500, 20, 200
