@@ -1,6 +1,7 @@
 # Build for the B200 FFTMatvec (sm_100a). `make` builds:
 #   paper_2508_10202_b200/libfftmv_cuda.so  -- the product (C ABI: include/fftmv_cuda.h)
 #   build/fftmv_cpp_tests                   -- C++ drop-in header tests (include/fftmv/*.hpp)
+#   build/fft_matvec                        -- command-line harness (SPEC.md cli module)
 #   oracle/liboracle.so, oracle/_ref/libfftmv_ref.so -- test-only checkers (oracle/Makefile)
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
@@ -8,7 +9,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC -Xcompiler -Wall --
 PKG := paper_2508_10202_b200
 SRC := $(wildcard $(PKG)/csrc/*.cu) $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.cpp) include/fftmv_cuda.h
 
-all: lib oracle cpp
+all: lib oracle cpp cli
 
 lib: $(PKG)/libfftmv_cuda.so
 
@@ -24,8 +25,14 @@ build/fftmv_cpp_tests: tests/cpp/test_dropin.cpp $(wildcard include/fftmv/*.hpp)
 	@mkdir -p build
 	g++ -std=c++20 -O2 -Wall -Iinclude -I/usr/local/cuda/include -I$(shell python -c "import sysconfig;print(sysconfig.get_paths()['purelib'])")/include/cudnn_frontend/thirdparty/nlohmann -o $@ tests/cpp/test_dropin.cpp -L$(PKG) -lfftmv_cuda -Wl,-rpath,'$$ORIGIN/../$(PKG)' -L/usr/local/cuda/lib64 -lcudart
 
+cli: build/fft_matvec
+
+build/fft_matvec: $(PKG)/cli/fft_matvec.cpp $(wildcard include/fftmv/*.hpp) include/fftmv_cuda.h $(PKG)/libfftmv_cuda.so
+	@mkdir -p build
+	g++ -std=c++20 -O2 -Wall -Iinclude -I/usr/local/cuda/include -o $@ $(PKG)/cli/fft_matvec.cpp -L$(PKG) -lfftmv_cuda -Wl,-rpath,'$$ORIGIN/../$(PKG)' -L/usr/local/cuda/lib64 -lcudart
+
 clean:
-	rm -f $(PKG)/libfftmv_cuda.so build/fftmv_cpp_tests
+	rm -f $(PKG)/libfftmv_cuda.so build/fftmv_cpp_tests build/fft_matvec
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib oracle cpp clean
+.PHONY: all lib oracle cpp cli clean

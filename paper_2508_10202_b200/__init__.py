@@ -14,6 +14,8 @@ from .preclab import *  # noqa: F401,F403
 from .preclab import __all__ as _a3
 from .partition import *  # noqa: F401,F403
 from .partition import __all__ as _a4
+from .vector_io import *  # noqa: F401,F403
+from .vector_io import __all__ as _a5
 from ._capi import FmvError, LIB_PATH, lib  # noqa: F401
 
-__all__ = list(_a1) + list(_a2) + list(_a3) + list(_a4) + ["lib", "LIB_PATH"]
+__all__ = list(_a1) + list(_a2) + list(_a3) + list(_a4) + list(_a5) + ["lib", "LIB_PATH"]

@@ -19,6 +19,7 @@
 #include "fftmv/partition.hpp"
 #include "fftmv/random_fill.hpp"
 #include "fftmv/sweep.hpp"
+#include "fftmv/vector_io.hpp"
 
 using namespace fftmv;
 
@@ -157,8 +158,51 @@ static void gpu_checks() {
   EXPECT(std::find_if(rows.begin(), rows.end(), [&](auto& r) { return r.config == rep.chosen; })->rel_error <= 1e-5);
 }
 
+// FMV1 (include/fftmv/vector_io.hpp): round trips over every code, the named
+// errors, and a file for the Python side to compare byte for byte.
+static void fmv1_checks() {
+  int n = 0;
+  for (int lay = 0; lay < 2; ++lay)
+    for (int prec = 0; prec < 2; ++prec)
+      for (int dom = 0; dom < 2; ++dom) {
+        BlockVector v;
+        v.space_extent = 3 + lay;
+        v.time_extent = 5 + prec;
+        v.layout = lay ? Layout::TOSI : Layout::SOTI;
+        v.precision = prec ? Precision::Single : Precision::Double;
+        v.domain = dom ? Domain::Frequency : Domain::Time;
+        auto x = uniform_fill(v.scalar_count(), 100 + n++);
+        if (prec) v.f32.assign(x.begin(), x.end());
+        else v.f64 = x;
+        const BlockVector w = decode_vector(encode_vector(v));
+        EXPECT(w.space_extent == v.space_extent && w.time_extent == v.time_extent && w.layout == v.layout &&
+               w.precision == v.precision && w.domain == v.domain && w.f64 == v.f64 && w.f32 == v.f32);
+      }
+  auto throws = [](const std::string& s, const char* what) {
+    try {
+      (void)decode_vector(s);
+    } catch (const std::invalid_argument& e) {
+      return std::string(e.what()).find(what) != std::string::npos;
+    }
+    return false;
+  };
+  const std::string good = encode_vector(BlockVector::time_double(2, 3, uniform_fill(6, 7)));
+  EXPECT(throws("", "bad magic") && throws("FMV2" + good.substr(4), "bad magic"));
+  EXPECT(throws(good.substr(0, 20), "truncated file"));
+  EXPECT(throws(good.substr(0, good.size() - 8), "truncated/oversized") && throws(good + "x", "truncated/oversized"));
+  std::string bad = good;
+  bad[4 + 16] = 2;
+  EXPECT(throws(bad, "layout code out of range"));
+  if (const char* path = std::getenv("FMV1_OUT")) {
+    BlockVector v = BlockVector::time_double(4, 9, uniform_fill(36, 2025));
+    save_vector(path, v);
+    EXPECT(load_vector(path).f64 == v.f64);
+  }
+}
+
 int main(int argc, char** argv) {
   host_checks();
+  fmv1_checks();
   if (argc > 1 && std::strcmp(argv[1], "--gpu") == 0) gpu_checks();
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
