@@ -96,10 +96,18 @@ def test_cli_raw_save_sweep_partition(tmp_path):
     assert np.array_equal(ao.data, F.adjoint_matvec(op, F.uniform_fill(nd * nt, F.seed_stream(S, 2))).output.data)
     r = subprocess.run(args + ["-sweep", "-rand", "-raw", "-tol", "1e-5"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
-    parts = r.stdout.split("# adjoint")
-    for part in parts:
-        back = F.parse_sweep_csv(part)
+    sections = []
+    for line in r.stdout.splitlines():
+        if line.startswith("#"):
+            sections.append([line])
+        else:
+            sections[-1].append(line)
+    assert [sec[0].split()[1] for sec in sections] == ["forward", "adjoint"]
+    for sec in sections:
+        back = F.parse_sweep_csv("\n".join(sec))
         assert len(back) == 32 and back[0].config.render() == "ddddd" and back[0].rel_error == 0.0
+        chosen = sec[0].split("chosen=")[1].split()[0]
+        assert next(b for b in back if b.config.render() == chosen).rel_error <= 1e-5
     r = subprocess.run(args + ["-p", "4", "-prec", "dddds", "-s", str(tmp_path / "p4")], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     pf = F.load_vector(str(tmp_path / "p4" / "forward_output.fmv")).data
