@@ -489,6 +489,19 @@ __global__ void __launch_bounds__(256) k_c2r(const typename PT<C3>::cplx* __rest
 // exp(-2*pi*i*m/L) the legacy kernel uses), so both kernels compute the same
 // DFT; summation order differs (radix-10 vs 8/5 stages), rounding-level.
 // ======================================================================
+// cp.async (LDGSTS) helpers: global -> shared without register staging.
+__device__ __forceinline__ void cp_async(void* dst, const void* src, int bytes_valid, int size) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  if (size == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes_valid) : "memory");
+  else if (size == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(bytes_valid) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(bytes_valid) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 template <int RX, int NP>
 struct RegPlan {
   static constexpr int N = NP == 2 ? RX * RX : RX * RX * RX;
@@ -686,7 +699,7 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::
 // Phases 4-5 + reorder (as k_c2r) for TOSI input in[k*in_ks + s] and SOTI
 // output out[s*out_ss + t], t < nout; S series per CTA.
 template <int C3, int C4, class Tout, int RX, int NP, int S>
-__global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::NR <= 256 ? 4 : 2)
+__global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::NR <= 256 ? 5 : 2)
     k_c2r_reg(const typename PT<C3>::cplx* __restrict__ in, long in_ks, long nseries, int nout, bool vec,
               Tout* __restrict__ out, long out_ss, const typename PT<C3>::cplx* __restrict__ tw) {
   using R = typename PT<C3>::real;
@@ -701,30 +714,17 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::
   C* buf = sbuf + s * SS;
   const R inv_len = R(1) / (R)(2 * N);
 
-  // Load the N+1 bins of S series (bin-major runs of S), scale by 1/L in the
-  // working precision, drop Im of DC and Nyquist (fft.hpp:130-148).
-  {
-    constexpr int TOT = S * (N + 1);
-    constexpr int U = (TOT + T - 1) / T;
-    C v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = threadIdx.x + u * T;
-      const int k = e / S, si = e - k * S;
-      if (e < TOT && si < ns) v[u] = in[(long)k * in_ks + s0 + si];
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = threadIdx.x + u * T;
-      const int k = e / S, si = e - k * S;
-      if (e < TOT && si < ns) {
-        C X = v[u];
-        X.x = X.x * inv_len;
-        X.y = (k == 0 || k == N) ? R(0) : X.y * inv_len;
-        sbuf[si * SS + pidx<RX>(k)] = X;
-      }
-    }
+  // The N+1 bins of S series (bin-major runs of S in global memory) land in
+  // the series-major shared buffer through cp.async -- no register staging,
+  // which keeps the kernel at 4+ resident CTAs per SM; the 1/L scaling and
+  // Im(X0) = Im(XN) = 0 (fft.hpp:130-148) are applied in the pre-pass read.
+  for (int e = threadIdx.x; e < S * (N + 1); e += T) {
+    const int k = e / S, si = e - k * S;
+    const bool ok = si < ns;
+    cp_async(sbuf + si * SS + k, in + (long)k * in_ks + s0 + (ok ? si : 0), ok ? (int)sizeof(C) : 0, (int)sizeof(C));
   }
+  cp_async_commit();
+  cp_async_wait_all();
   __syncthreads();
   // Pre-pass fused into pass 1: Z[n] = (X[n] + conj X[N-n]) + i w^-n (X[n] - conj X[N-n]).
   {
@@ -734,8 +734,11 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::
 #pragma unroll
       for (int q = 0; q < RX; ++q) {
         const int n = j + q * NR;
-        const C A = buf[pidx<RX>(n)];
-        const C B = cconj(buf[pidx<RX>(N - n)]);
+        C A = buf[pidx<RX>(n)], B = buf[pidx<RX>(N - n)];  // X[n], X[N-n]
+        A.x = A.x * inv_len;
+        A.y = n == 0 ? R(0) : A.y * inv_len;  // Im(X0) = 0
+        B.x = B.x * inv_len;
+        B.y = n == 0 ? -R(0) : -(B.y * inv_len);  // conj; Im(XN) = 0 (sign of zero as cconj(0))
         C w;  // w^n = w^j * w^(q*N/RX); for RX = 10 the second factor is a constant
         if constexpr (RX == 10) w = q == 0 ? wj : cmul(wj, half_turn10<R>(q));
         else w = __ldg(tw + n);
