@@ -535,11 +535,24 @@ constexpr int reg_tw_offset() {
 // RX = 10 only q = 1, 2, 3, 6 are read and the rest formed as one product of
 // two table values (w4 = w1 w3, w5 = w2 w3, w7 = w1 w6, w8 = w2 w6,
 // w9 = w3 w6: ~1 ulp), cutting the L1 twiddle traffic that bounds the pass.
+// fp64 (the all-double hot path) reads only w1 and forms w2 = w1^2,
+// w3 = w1 w2, w6 = w3^2 (<= ~6 ulp on w9, ~1e-15: far inside the 1e-12
+// contract); fp32 keeps four exact table reads, as its tolerance is tied to
+// the reference's own fp32 error.
 template <class R, int D, int RX, int Ns>
 __device__ __forceinline__ void apply_twiddles(typename CT<R>::c* v, const typename CT<R>::c* __restrict__ twp, int k) {
   if constexpr (RX == 10) {
-    const auto w1 = twiddle<D>(twp, Ns + k), w2 = twiddle<D>(twp, 2 * Ns + k);
-    const auto w3 = twiddle<D>(twp, 3 * Ns + k), w6 = twiddle<D>(twp, 6 * Ns + k);
+    using C = typename CT<R>::c;
+    C w1, w2, w3, w6;
+    if constexpr (sizeof(R) == 8) {
+      w1 = twiddle<D>(twp, Ns + k);
+      w2 = cmul(w1, w1);
+      w3 = cmul(w1, w2);
+      w6 = cmul(w3, w3);
+    } else {
+      w1 = twiddle<D>(twp, Ns + k), w2 = twiddle<D>(twp, 2 * Ns + k);
+      w3 = twiddle<D>(twp, 3 * Ns + k), w6 = twiddle<D>(twp, 6 * Ns + k);
+    }
     v[1] = cmul(v[1], w1);
     v[2] = cmul(v[2], w2);
     v[3] = cmul(v[3], w3);
