@@ -317,6 +317,14 @@ def run_ours(args, rank, world, local_rank):
     if kn[3]:
         detail["c2r_all_ms_per_step"] = kms[3] / args.steps
     detail["fft_big_phase_bytes"] = {"r2c_F": r2c_bytes, "c2r_Fstar": c2r_bytes}
+    # FFT phase (all r2c + c2r launches of a step: F's big r2c and small c2r,
+    # F*'s small r2c and big c2r) as HBM GB/s against the same peak
+    small = ND * NT * 8 + ND * nb * es + ND * nb * 16 + ND * NT * 8
+    if kn[0] and kn[3]:
+        t_fft = (kms[0] + kms[3]) / args.steps * 1e-3
+        fb = r2c_bytes + c2r_bytes + small
+        detail["fft_phase"] = {"bytes_per_step": fb, "ms_per_step": t_fft * 1e3, "gbs": fb / t_fft / 1e9,
+                               "frac": fb / t_fft / 1e9 / peak}
     share = (kms[1] + kms[2]) / ms if ms > 0 else None
     traffic = None
     nc = ncu_traffic()
@@ -338,9 +346,42 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roofline,
         "clocks": clk.summary(),
     }
+    if world == 1 and not args.no_block and cfg[2] in "ds":
+        line["block"] = block_throughput(F, L, ctx, op, cfg, m_h, d_h, dev, stream)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(col, m_h, d_h, cfg)
     return line
+
+
+def block_throughput(F, L, ctx, op, cfg, m_h, d_h, dev, stream, reps=5):
+    """Extra (not the headline): the block (multi-RHS) matvec, SURVEY.md §8 f2 --
+    K right-hand sides per call (8 for F, 4 for F*), the operator streamed once
+    per call; device-resident I/O, per-RHS matvecs/s, CUDA events."""
+    import torch
+
+    from paper_2508_10202_b200 import _capi
+
+    out = {}
+    for kind, K, x_h, n_out in ((0, 8, m_h, ND * NT), (1, 4, d_h, NM * NT)):
+        X = torch.from_numpy(np.tile(x_h, K)).to(dev)
+        Y = torch.empty(K * n_out, dtype=torch.float64, device=dev)
+
+        def call():
+            _capi.check(L.fmv_matvec_block_async(ctx.handle, op.handle, kind, cfg.encode(), K,
+                                                 ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(Y.data_ptr())))
+        for _ in range(2):
+            call()
+        ctx.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            call()
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        out["F" if kind == 0 else "Fstar"] = {"rhs_per_call": K, "ms_per_call": ms, "matvecs_per_s": K / (ms * 1e-3)}
+    out["note"] = "extra: block matvec (fmv_matvec_block), operator read once per call; not the headline value"
+    return out
 
 
 def cpu_baseline(col, m, d, cfg):
@@ -365,6 +406,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cfg", default="ddddd")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-block", action="store_true", help="skip the block (multi-RHS) extra measurement")
     ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
                     help="c2: Nm=5000, Nd=100, Nt=1000 per GPU (default); c5: Nd=600 (48 GB fp64 operator per GPU)")
     args = ap.parse_args()
