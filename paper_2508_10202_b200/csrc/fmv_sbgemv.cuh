@@ -347,7 +347,10 @@ __device__ __forceinline__ void neumaier_add(A& s, A& c, A x) {
 }
 
 template <int MODE, class E, class O, int RPT, int V, int LPC>
-__global__ void __launch_bounds__(288, 2) k_sbgemv(const GemvParams p) {
+#ifndef FMV_SBGEMV_MINB
+#define FMV_SBGEMV_MINB 2  // resident CTAs per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__(288, FMV_SBGEMV_MINB) k_sbgemv(const GemvParams p) {
   using Tr = ET<E>;
   using Acc = typename Tr::A;
   extern __shared__ __align__(128) unsigned char sm[];
