@@ -963,7 +963,7 @@ bool plan_block(GemvPlan& gp, int mode, size_t es, size_t accsz, int KR) {
     if ((long)gp.smem <= budget || Jc == 1) break;
     Jc = std::max(1, Jc * 3 / 4);
   }
-  p.arrive_all = 0;
+  p.arrive_all = env_int("FMV_SBGEMV_ARRIVE_ALL", 0);  // racecheck mode, as k_sbgemv
   return gp.smem <= 227 * 1024 && (long)(p.Jc - 1) * p.lda * (long)es + p.m * (long)es <= 96 * 1024;
 }
 

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(288, 2) k_sbgemm_block(const GemvParams p) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.nstage; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], ncons / 32);
+      mbar_init(&empty[s], p.arrive_all ? ncons : ncons / 32);
     }
     mbar_fence_init();
   }
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(288, 2) k_sbgemm_block(const GemvParams p) {
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (p.arrive_all || lane == 0) mbar_arrive(&empty[s]);
       if (sg.ends_bin(p)) {
         const int KM = K * p.m;
         if (active) {
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(288, 2) k_sbgemm_block(const GemvParams p) {
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (p.arrive_all || lane == 0) mbar_arrive(&empty[s]);
     }
   }
 }
