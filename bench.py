@@ -217,7 +217,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     stream = torch.cuda.ExternalStream(ctx.stream_ptr, device=dev)
     dm = None
-    if world > 1:
+    if world > 1 or os.environ.get("FMV_BENCH_FORCE_DIST") == "1":  # (the latter: exercise the NCCL path on 1 GPU)
         dm = F.DistributedMatvec(F.ProblemDims(NM * world, ND, NT), rank, world, shard=op, transport="native", ctx=ctx)
 
     def step_device():

@@ -1153,7 +1153,7 @@ std::pair<const void*, int> bcast_payload(fmv_ctx* ctx, void* comm, int gsize, b
                                           int p0) {
   cudaStream_t s = ctx->stream;
   if (p0 == PD) {
-    if (gsize == 1) return {in, PD};
+    if (!comm) return {in, PD};
     ctx->payload.ensure(n * sizeof(double));
     if (root) CK(cudaMemcpyAsync(ctx->payload.p, in, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     nck(nccl().broadcast(ctx->payload.p, ctx->payload.p, n, kNcclDouble, 0, comm, s), "ncclBroadcast");
@@ -1167,7 +1167,7 @@ std::pair<const void*, int> bcast_payload(fmv_ctx* ctx, void* comm, int gsize, b
       launch(ctx, 4, [&] { k_d2h<<<grid_for(n, 256, ctx->device), 256, 0, s>>>(in, static_cast<__half*>(ctx->payload.p), n); });
     g_casts.fetch_add(1, std::memory_order_relaxed);  // partition.hpp:203
   }
-  if (gsize > 1)
+  if (comm)
     nck(nccl().broadcast(ctx->payload.p, ctx->payload.p, n, p0 == PS ? kNcclFloat : kNcclHalf, 0, comm, s),
         "ncclBroadcast");
   return {ctx->payload.p, p0};
@@ -1175,7 +1175,7 @@ std::pair<const void*, int> bcast_payload(fmv_ctx* ctx, void* comm, int gsize, b
 
 // Sum the n-double partial `buf` over `comm` in cfg[4] precision (partition.hpp:175-177).
 void allreduce_prec(fmv_ctx* ctx, void* comm, int gsize, double* buf, long n, int p4) {
-  if (gsize == 1) return;
+  if (!comm) return;
   cudaStream_t s = ctx->stream;
   if (p4 == PD) {
     nck(nccl().all_reduce(buf, buf, n, kNcclDouble, kNcclSum, comm, s), "ncclAllReduce");
@@ -1552,8 +1552,12 @@ int fmv_comm_init(fmv_ctx* ctx, int nranks, int rank, const void* id128) {
     DeviceGuard dg(ctx->device);
     ctx->nranks = nranks;
     ctx->rank = rank;
-    if (nranks == 1) return;
-    if (!id128) fail(FMV_EINVAL, "fmv_comm_init: null unique id");
+    // A single rank needs no communicator; given an id it still builds one
+    // (NCCL supports 1-rank communicators), so the collectives run for real.
+    if (!id128) {
+      if (nranks == 1) return;
+      fail(FMV_EINVAL, "fmv_comm_init: null unique id");
+    }
     struct Id {
       char b[128];
     } id;
@@ -1588,7 +1592,7 @@ int fmv_comm_init_2d(fmv_ctx* ctx, int pr, int pc, int rank, const void* id128) 
     ctx->pc = pc;
     ctx->ri = rank / pc;
     ctx->cj = rank % pc;
-    if (pr * pc == 1) return;
+    if (!ctx->comm) return;  // single rank without a communicator
     if (!nccl().comm_split) fail(FMV_ENCCL, "ncclCommSplit is not available in the loaded NCCL");
     nck(nccl().comm_split(ctx->comm, ctx->ri, ctx->cj, &ctx->row_comm, nullptr), "ncclCommSplit(row)");
     nck(nccl().comm_split(ctx->comm, ctx->cj, ctx->ri, &ctx->col_comm, nullptr), "ncclCommSplit(col)");
@@ -1624,7 +1628,7 @@ int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* op, int kind, const char*
       // partition.hpp:157-182: full-length partial d per rank, summed in cfg[4].
       pipeline(ctx, op, kind, p, din, -1, dout);
       if (times) CK(cudaEventRecord(te[2], s));
-      if (ctx->nranks > 1) {
+      if (ctx->comm) {
         const long nd = (long)(op->nd * nt);
         if (p[4] == PD) {
           nck(nccl().all_reduce(dout, dout, nd, kNcclDouble, kNcclSum, ctx->comm, s), "ncclAllReduce");
@@ -1643,7 +1647,7 @@ int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* op, int kind, const char*
       const void* pay = din;
       int pprec = PD;
       if (p[0] == PD) {
-        if (ctx->nranks > 1) {
+        if (ctx->comm) {
           ctx->payload.ensure(nd * sizeof(double));
           if (ctx->rank == 0)
             CK(cudaMemcpyAsync(ctx->payload.p, din, nd * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -1663,7 +1667,7 @@ int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* op, int kind, const char*
             });
           g_casts.fetch_add(1, std::memory_order_relaxed);  // partition.hpp:203
         }
-        if (ctx->nranks > 1)
+        if (ctx->comm)
           nck(nccl().broadcast(ctx->payload.p, ctx->payload.p, nd, p[0] == PS ? kNcclFloat : kNcclHalf, 0, ctx->comm,
                                s),
               "ncclBroadcast");

@@ -218,10 +218,12 @@ class DistributedMatvec:
     def _init_native(self):
         import torch.distributed as dist
 
+        # rank 0's NCCL id, shipped with torch.distributed (a 1-rank run still
+        # builds a real 1-rank communicator, so the collectives execute)
         idb = (ctypes.c_char * 128)()
+        if self.rank == 0:
+            check(lib().fmv_comm_unique_id(idb))
         if self.world > 1:
-            if self.rank == 0:
-                check(lib().fmv_comm_unique_id(idb))
             obj = [bytes(idb)] if self.rank == 0 else [None]
             dist.broadcast_object_list(obj, src=0)
             idb = (ctypes.c_char * 128).from_buffer_copy(obj[0])
@@ -426,9 +428,9 @@ class DistributedMatvec2D:
             import torch.distributed as dist
 
             idb = (ctypes.c_char * 128)()
+            if rank == 0:
+                check(lib().fmv_comm_unique_id(idb))
             if self.grid.size > 1:
-                if rank == 0:
-                    check(lib().fmv_comm_unique_id(idb))
                 obj = [bytes(idb)] if rank == 0 else [None]
                 dist.broadcast_object_list(obj, src=0)
                 idb = (ctypes.c_char * 128).from_buffer_copy(obj[0])
