@@ -581,7 +581,7 @@ void sbgemv_launch_t(fmv_ctx* ctx, GemvPlan& gp) {
     }
   }
   if (occ < 1) fail(FMV_EUNSUPPORTED, "sbgemv: staged kernel does not fit on an SM");
-  const int ctas_per_sm = std::min(occ, env_int("FMV_SBGEMV_CTAS_PER_SM", 2));
+  const int ctas_per_sm = std::min(occ, env_int("FMV_SBGEMV_CTAS_PER_SM", FMV_SBGEMV_MINB));
   long P = (long)sm_count(ctx->device) * ctas_per_sm;
   P = std::min(P, gp.p.T);
   gp.p.P = (int)P;
@@ -601,7 +601,8 @@ void sbgemv_simple_t(fmv_ctx* ctx, GemvPlan& gp) {
   launch(ctx, MODE == GM_N ? 1 : 2, [&] { k_sbgemv_simple<MODE, E, O><<<grid, 128, 0, ctx->stream>>>(gp.p); });
 }
 
-constexpr int kConsumers = 256;  // consumer threads per CTA (+1 producer warp); __launch_bounds__(288, 2)
+constexpr int kConsumers = FMV_SBGEMV_CONS;  // k_sbgemv consumer threads per CTA (+1 producer warp)
+constexpr int kBlockConsumers = 256;          // k_sbgemm_block: __launch_bounds__(288, 2)
 
 // Fills the staged-kernel plan for V-element (16-byte) row vectors; returns
 // false when the staged kernel's limits are exceeded (NoTrans: m > 4*256*V
@@ -610,8 +611,9 @@ bool plan_staged(GemvPlan& gp, int mode, size_t es, size_t accsz, int V) {
   GemvParams& p = gp.p;
   const long col_bytes = p.lda * (long)es;
   const int MV0 = (p.m + V - 1) / V;
-  int a_target = 32 * 1024;
-  int nst = 3;
+  // short columns: NoTrans 4 x 32 KB, (Conj)Trans 3 x 48 KB (one CTA per SM; tools/ab_wide.sh)
+  int a_target = mode == GM_N ? 32 * 1024 : 48 * 1024;
+  int nst = mode == GM_N ? 4 : 3;
   if (mode != GM_N && MV0 > 128) {
     // tall (Conj)Trans columns: 64-96 KB stages (>= ~6 columns), one warp per
     // column, 3 stages when they fit the 227 KB per-CTA limit, else 2, shrunk
@@ -936,7 +938,7 @@ inline int block_max(bool fwd) { return fwd ? kBlockMax : 4; }
 // two CTAs fit an SM; false if the shape is outside the kernel's limits.
 bool plan_block(GemvPlan& gp, int mode, size_t es, size_t accsz, int KR) {
   GemvParams& p = gp.p;
-  if (p.m < 1 || (mode == GM_N && p.m > kConsumers)) return false;
+  if (p.m < 1 || (mode == GM_N && p.m > kBlockConsumers)) return false;
   auto up128 = [](long v) { return (int)((v + 127) / 128 * 128); };
   const long col_bytes = std::max<long>(1, p.lda * (long)es);
   const long budget = 110 * 1024;
@@ -945,10 +947,10 @@ bool plan_block(GemvPlan& gp, int mode, size_t es, size_t accsz, int KR) {
   size_t red = 0;
   if (mode == GM_N) {
     p.RT = p.m;
-    p.G = std::max(1, kConsumers / p.RT);
+    p.G = std::max(1, kBlockConsumers / p.RT);
     gp.block = (p.RT * p.G + 31) / 32 * 32 + 32;
   } else {
-    gp.block = kConsumers + 32;
+    gp.block = kBlockConsumers + 32;
   }
   for (;;) {
     const long max_a = ((long)(Jc - 1) * p.lda + p.m) * (long)es;
@@ -1010,7 +1012,7 @@ bool sbgemm_block_e(fmv_ctx* ctx, int p3, int mode, GemvPlan& gp) {
 // nd > 256 rows run as K single-RHS pipelines instead.)
 bool block_supported(const fmv_op* op, int kind, const std::array<int, 5>& p) {
   if (p[2] == PH) return false;
-  return kind != FMV_FORWARD || op->nd <= (size_t)kConsumers;
+  return kind != FMV_FORWARD || op->nd <= (size_t)kBlockConsumers;
 }
 
 // run_pipeline over K right-hand sides: in = K SOTI vectors back to back

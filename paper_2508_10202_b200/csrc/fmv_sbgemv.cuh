@@ -347,10 +347,17 @@ __device__ __forceinline__ void neumaier_add(A& s, A& c, A x) {
 }
 
 template <int MODE, class E, class O, int RPT, int V, int LPC>
+// One CTA per SM with 16 consumer warps: measured at C2 (tools/ab_wide.sh) it
+// streams 5-6% faster than two 8-warp CTAs per SM -- half as many concurrent
+// DRAM streams with the same consumer width (the bare TMA ring shows the same
+// 1-vs-2 CTA effect, tools/read_ceiling.cu).
 #ifndef FMV_SBGEMV_MINB
-#define FMV_SBGEMV_MINB 2  // resident CTAs per SM the register budget is sized for
+#define FMV_SBGEMV_MINB 1  // resident CTAs per SM the register budget is sized for
 #endif
-__global__ void __launch_bounds__(288, FMV_SBGEMV_MINB) k_sbgemv(const GemvParams p) {
+#ifndef FMV_SBGEMV_CONS
+#define FMV_SBGEMV_CONS 512  // consumer threads per CTA (+ one producer warp)
+#endif
+__global__ void __launch_bounds__(FMV_SBGEMV_CONS + 32, FMV_SBGEMV_MINB) k_sbgemv(const GemvParams p) {
   using Tr = ET<E>;
   using Acc = typename Tr::A;
   extern __shared__ __align__(128) unsigned char sm[];

@@ -85,11 +85,33 @@ __global__ void __launch_bounds__(288) k_bulk(const unsigned char* __restrict__ 
       const int s = i % NS;
       mbar_wait(full + s, (i / NS) & 1);
       const double2* st = reinterpret_cast<const double2*>(ring + (long)s * SB);
-      if (consume) {
+      if (consume == 1) {
         for (int k = threadIdx.x; k < SB / 16; k += NC) {
           const double2 v = st[k];
           acc = fma(v.x, v.y, acc);
         }
+      } else if (consume == 2) {  // a complex MAC per element (4 DFMA), as the NoTrans SBGEMV
+        double2 c = make_double2(acc, 0.0);
+        const double2 xv = st[threadIdx.x & 7];
+        for (int k = threadIdx.x; k < SB / 16; k += NC) {
+          const double2 v = st[k];
+          c.x = fma(v.x, xv.x, c.x);
+          c.x = fma(-v.y, xv.y, c.x);
+          c.y = fma(v.x, xv.y, c.y);
+          c.y = fma(v.y, xv.x, c.y);
+        }
+        acc = c.x + c.y;
+      } else if (consume == 3) {  // + a broadcast x load per element
+        double2 c = make_double2(acc, 0.0);
+        for (int k = threadIdx.x; k < SB / 16; k += NC) {
+          const double2 v = st[k];
+          const double2 xv = st[(k / 100) & 31];
+          c.x = fma(v.x, xv.x, c.x);
+          c.x = fma(-v.y, xv.y, c.x);
+          c.y = fma(v.x, xv.y, c.y);
+          c.y = fma(v.y, xv.x, c.y);
+        }
+        acc = c.x + c.y;
       } else if (threadIdx.x % 32 == 0) {
         acc += st[threadIdx.x].x;
       }
@@ -119,7 +141,7 @@ int main() {
     cudaEventCreate(&e1);
     float ms;
     for (int blk : {512}) {
-      for (int per_sm : {2, 8}) {
+      for (int per_sm : {8}) {
         const int grid = nsm * per_sm;
         for (int w = 0; w < 2; ++w) k_ldg<<<grid, blk>>>((const double2*)a, bytes / 16, out);
         cudaEventRecord(e0);
@@ -131,8 +153,8 @@ int main() {
       }
     }
     struct Cfg { int SB, NS, per_sm, pol, consume; };
-    const Cfg cfgs[] = {{32768, 3, 2, 0, 0}, {32000, 3, 2, 0, 0}, {32768, 3, 2, 1, 0}, {32768, 3, 2, 0, 1},
-                        {32000, 3, 2, 1, 1}, {16384, 6, 2, 0, 1}, {32768, 3, 1, 0, 1}, {65536, 3, 1, 0, 1}};
+    const Cfg cfgs[] = {{32768, 3, 2, 0, 0}, {32768, 3, 2, 0, 1}, {32768, 3, 2, 0, 2}, {32768, 3, 2, 0, 3},
+                        {32768, 3, 2, 1, 2}, {16384, 6, 2, 0, 2}, {24576, 4, 2, 0, 2}, {32768, 3, 1, 0, 2}};
     for (const Cfg& c : cfgs) {
       const size_t smem = 256 + (size_t)c.SB * c.NS;
       cudaFuncSetAttribute(k_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -17,7 +17,10 @@ torch.cuda.synchronize()
 L = F.lib()
 nb = NT + 1
 grid = [(st, sb, cps) for st in (3, 4, 6, 8) for sb in (16384, 24576, 32768, 49152) for cps in (1, 2)]
-if len(sys.argv) > 2 and sys.argv[2] == "quick":
+if len(sys.argv) > 2 and sys.argv[2] == "env":  # one row from the caller's FMV_SBGEMV_* environment
+    grid = [(int(os.environ.get("FMV_SBGEMV_STAGES", 3)), int(os.environ.get("FMV_SBGEMV_STAGE_BYTES", 32768)),
+             int(os.environ.get("FMV_SBGEMV_CTAS_PER_SM", 2)))]
+elif len(sys.argv) > 2 and sys.argv[2] == "quick":
     grid = [(4, 24576, 2), (6, 16384, 2), (8, 12288, 2), (3, 32768, 2), (8, 24576, 1)]
 for cfg in cfgs:
     es = {"d": 16, "s": 8, "h": 4}[cfg[2]]
