@@ -611,9 +611,12 @@ bool plan_staged(GemvPlan& gp, int mode, size_t es, size_t accsz, int V) {
   GemvParams& p = gp.p;
   const long col_bytes = p.lda * (long)es;
   const int MV0 = (p.m + V - 1) / V;
-  // short columns: NoTrans 4 x 32 KB, (Conj)Trans 3 x 48 KB (one CTA per SM; tools/ab_wide.sh)
-  int a_target = mode == GM_N ? 32 * 1024 : 48 * 1024;
-  int nst = mode == GM_N ? 4 : 3;
+  // short columns (one CTA per SM; tools/ab_wide.sh, tools/ab_half.sh): 3 x 48 KB,
+  // except fp64 NoTrans 4 x 32 KB (fp16 NoTrans at 4 x 32 KB drops to 5.5 TB/s:
+  // too few columns per thread per stage for its per-stage compensated fold)
+  const bool n64 = mode == GM_N && es == 16;
+  int a_target = n64 ? 32 * 1024 : 48 * 1024;
+  int nst = n64 ? 4 : 3;
   if (mode != GM_N && MV0 > 128) {
     // tall (Conj)Trans columns: 64-96 KB stages (>= ~6 columns), one warp per
     // column, 3 stages when they fit the 227 KB per-CTA limit, else 2, shrunk
