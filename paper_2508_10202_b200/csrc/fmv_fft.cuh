@@ -635,7 +635,7 @@ struct IPow<0, RX> {
 // Phases 1-2 + reorder (as k_r2c) for SOTI input in[s*in_ss + t] and TOSI
 // output out[k*out_ks + s]; S series per CTA.
 template <int C0, int C1, int C2, class Tin, int RX, int NP, int S>
-__global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::NR <= 256 ? 4 : 2)
+__global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::NR <= 256 ? 5 : 2)
     k_r2c_reg(const Tin* __restrict__ in, long in_ss, long nseries, int nvalid, bool vec,
               typename PT<C2>::cplx* __restrict__ out, long out_ks,
               const typename CT<typename PT<C1>::real>::c* __restrict__ tw) {
