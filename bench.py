@@ -32,6 +32,8 @@ import threading
 import time
 
 os.environ.setdefault("MKL_NUM_THREADS", "1")
+# NCCL prints its version banner on stdout at init; keep stdout for the one JSON line
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 

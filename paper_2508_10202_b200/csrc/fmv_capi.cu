@@ -1642,17 +1642,24 @@ int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* op, int kind, const char*
     double* dout = out;
     const bool have_in = fwd || ctx->rank == 0;
     if (have_in && !in) fail(FMV_EINVAL, "fmv_matvec_partitioned: null input");
+    // Host I/O without PhaseTimings: the shard pipeline overlaps the big copy
+    // with its SBGEMV column chunks (F: the m slice in; F*: the m slice out),
+    // as fmv_matvec does.
+    const bool chunked = !io_on_device && !times;
+    HostIO hio{};
     if (!io_on_device) {
       ctx->io_in.ensure(std::max(n_in, op->nd * nt) * sizeof(double));
       ctx->io_out.ensure(n_out * sizeof(double));
-      if (have_in) CK(cudaMemcpyAsync(ctx->io_in.p, in, n_in * sizeof(double), cudaMemcpyHostToDevice, s));
+      if (chunked && fwd) hio.h_in = in;
+      else if (have_in) CK(cudaMemcpyAsync(ctx->io_in.p, in, n_in * sizeof(double), cudaMemcpyHostToDevice, s));
+      if (chunked && !fwd) hio.h_out = out;
       din = static_cast<const double*>(ctx->io_in.p);
       dout = static_cast<double*>(ctx->io_out.p);
     }
     if (times) CK(cudaEventRecord(te[1], s));
     if (fwd) {
       // partition.hpp:157-182: full-length partial d per rank, summed in cfg[4].
-      pipeline(ctx, op, kind, p, din, -1, dout);
+      pipeline(ctx, op, kind, p, din, -1, dout, nullptr, nullptr, chunked ? &hio : nullptr);
       if (times) CK(cudaEventRecord(te[2], s));
       if (ctx->comm) {
         const long nd = (long)(op->nd * nt);
@@ -1701,10 +1708,11 @@ int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* op, int kind, const char*
         pprec = p[0];
       }
       if (times) CK(cudaEventRecord(te[2], s));
-      pipeline(ctx, op, kind, p, pay, pprec, dout);
+      pipeline(ctx, op, kind, p, pay, pprec, dout, nullptr, nullptr, chunked ? &hio : nullptr);
       if (times) CK(cudaEventRecord(te[3], s));
     }
-    if (!io_on_device) CK(cudaMemcpyAsync(out, dout, n_out * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (!io_on_device && !(chunked && !fwd))  // (chunked F*: the pipeline already copied the slice out)
+      CK(cudaMemcpyAsync(out, dout, n_out * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (times) CK(cudaEventRecord(te[4], s));
     CK(cudaStreamSynchronize(s));
     if (times) {
