@@ -602,7 +602,7 @@ void sbgemv_simple_t(fmv_ctx* ctx, GemvPlan& gp) {
 }
 
 constexpr int kConsumers = FMV_SBGEMV_CONS;  // k_sbgemv consumer threads per CTA (+1 producer warp)
-constexpr int kBlockConsumers = 256;          // k_sbgemm_block: __launch_bounds__(288, 2)
+constexpr int kBlockConsumers = FMV_BLOCK_CONS;  // k_sbgemm_block consumer threads per CTA
 
 // Fills the staged-kernel plan for V-element (16-byte) row vectors; returns
 // false when the staged kernel's limits are exceeded (NoTrans: m > 4*256*V
@@ -965,9 +965,9 @@ bool plan_block(GemvPlan& gp, int mode, size_t es, size_t accsz, int KR) {
   if (p.m < 1 || (mode == GM_N && p.m > kBlockConsumers)) return false;
   auto up128 = [](long v) { return (int)((v + 127) / 128 * 128); };
   const long col_bytes = std::max<long>(1, p.lda * (long)es);
-  const long budget = 110 * 1024;
+  const long budget = FMV_BLOCK_MINB >= 2 ? 110 * 1024 : 220 * 1024;  // fit FMV_BLOCK_MINB CTAs per SM
   p.nstage = 3;
-  int Jc = (int)std::max<long>(1, 32768 / col_bytes);
+  int Jc = (int)std::max<long>(1, env_int("FMV_BLOCK_STAGE_BYTES", FMV_BLOCK_MINB >= 2 ? 32768 : 65536) / col_bytes);
   size_t red = 0;
   if (mode == GM_N) {
     p.RT = p.m;
@@ -1000,7 +1000,7 @@ void sbgemm_block_launch_t(fmv_ctx* ctx, GemvPlan& gp) {
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, gp.block, gp.smem));
   if (occ < 1) fail(FMV_EUNSUPPORTED, "block sbgemv: kernel does not fit on an SM");
-  long P = (long)sm_count(ctx->device) * std::min(occ, 2);
+  long P = (long)sm_count(ctx->device) * std::min(occ, FMV_BLOCK_MINB);
   P = std::min(P, gp.p.T);
   gp.p.P = (int)P;
   if (MODE == GM_N) {

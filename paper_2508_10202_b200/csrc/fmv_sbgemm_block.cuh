@@ -28,8 +28,16 @@
 
 namespace fmv {
 
+// One 16-warp CTA per SM with ~64 KB stages, as k_sbgemv: at C2 fp64 F K = 8
+// goes 2949 -> 3190 RHS/s against two 8-warp CTAs per SM (tools/ab_block.sh).
+#ifndef FMV_BLOCK_CONS
+#define FMV_BLOCK_CONS 512  // consumer threads per CTA (+ one producer warp)
+#endif
+#ifndef FMV_BLOCK_MINB
+#define FMV_BLOCK_MINB 1  // resident CTAs per SM
+#endif
 template <int MODE, class E, class O, int KR, int LPC>
-__global__ void __launch_bounds__(288, 2) k_sbgemm_block(const GemvParams p) {
+__global__ void __launch_bounds__(FMV_BLOCK_CONS + 32, FMV_BLOCK_MINB) k_sbgemm_block(const GemvParams p) {
   using Tr = ET<E>;
   using Acc = typename Tr::A;
   extern __shared__ __align__(128) unsigned char sm[];
