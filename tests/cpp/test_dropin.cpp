@@ -139,6 +139,17 @@ static void gpu_checks() {
       EXPECT(relative_error(BA[r].f64, adjoint_matvec(op, ds[r], PrecisionConfig{}).output.f64) <= 1e-14);
     }
   }
+  // 2-D grid at 1 x 1 through NCCL (a real 1-rank communicator): equals the serial matvec bitwise
+  {
+    auto g = GridPxQ::split(2, 3, dims.n_d, dims.n_m);
+    auto shards = shard_operator_2d(col, g);
+    EXPECT(shards.size() == 6 && shards[4].dims.n_d == 2 && shards[4].dims.n_m == 5 && g.coords(4).second == 1);
+    EXPECT(shards[4].at(3, 1, 2) == col.at(3, g.row_ranges[1].first + 1, g.col_ranges[1].first + 2));
+    NcclGrid2D grid(1, 1, 0, NcclPartition::unique_id());
+    const auto gf = grid.forward(op, m, PrecisionConfig{});
+    const auto ga = grid.adjoint(op, d, PrecisionConfig{});
+    EXPECT(gf == F.output.f64 && ga == A.output.f64);
+  }
   // FFT facade round trip
   FftPlan fwd(16, 3, Precision::Double, FftDirection::Forward), inv(16, 3, Precision::Double, FftDirection::Inverse);
   auto x = uniform_fill(48, 3);
