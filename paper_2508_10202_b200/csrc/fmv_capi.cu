@@ -925,9 +925,10 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
     if (ev_r2c) CK(cudaEventRecord(ev_r2c, cs));
     if (h_out) {
       cudaStream_t ks = copy_stream(ctx);
-      // (chunk c's c2r stays on the matvec stream: issued on the copy stream it
-      // becomes eligible together with the SBGEMV of chunk c+1, floods the SMs
-      // and delays the persistent SBGEMV CTAs -- measured 1.37 -> 1.62 ms)
+      // (chunk c's c2r stays on the matvec stream: on the copy stream, running
+      // alongside the SBGEMV of chunk c+1, it slowed F* from 1.37 to 1.62 ms
+      // with a full grid and to 2.13 ms with one-CTA-per-SM sub-launches --
+      // the c2r's shared-memory traffic competes with the ConjTrans consumers)
       for (int c = 0; c < C; ++c) {
         const long j0 = chunk_edge(n, c, C), j1 = chunk_edge(n, c + 1, C);
         gemv_chunk(c);
