@@ -111,6 +111,20 @@ int fmv_matvec_block(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, 
 int fmv_matvec_block_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, size_t nrhs, const double* d_in,
                            double* d_out);
 
+/* ---- CUDA-graph matvec (device-resident I/O) ----
+ * Captures one fmv_matvec_async(ctx, op, kind, cfg, d_in, d_out) into a CUDA
+ * graph (after one warm-up run that sizes a private workspace); each
+ * fmv_graph_launch replays it on ctx's stream with a single cudaGraphLaunch,
+ * reading d_in and writing d_out as they are at replay time. For iterative
+ * solvers that apply F / F* many times to the same buffers, and small,
+ * launch-bound problems. The graph owns its workspace, so it stays valid
+ * whatever else runs on ctx; destroy it before freeing d_in / d_out. */
+typedef struct fmv_graph fmv_graph;
+int fmv_graph_create(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* d_in, double* d_out,
+                     fmv_graph** out);
+int fmv_graph_launch(fmv_graph* g);
+int fmv_graph_destroy(fmv_graph* g);
+
 /* ---- batched real FFTs (fft.hpp:110-148), device pointers ----
  * r2c: batch contiguous series of L reals -> batch x (L/2+1) complex bins,
  *      unnormalized, sign -1. c2r: the true inverse, 1/L folded in by

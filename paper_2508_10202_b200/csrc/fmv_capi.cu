@@ -1781,4 +1781,83 @@ int fmv_matvec_partitioned_2d(fmv_ctx* ctx, const fmv_op* op, int kind, const ch
   });
 }
 
+// ---- CUDA-graph matvec: one device-resident matvec captured once, replayed
+// with a single cudaGraphLaunch (iterative solvers applying F / F* many times
+// to the same buffers; small problems are launch-bound). The graph owns a
+// private workspace context, so later calls on the caller's context cannot
+// move buffers the graph's kernels point at.
+struct fmv_graph {
+  fmv_ctx* wctx = nullptr;  // private workspace + capture stream
+  cudaStream_t stream = nullptr;  // the caller's ctx stream (replays run there)
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t casts = 0;  // logical casts per matvec (precision.hpp:27-39), ticked per replay
+  int device = 0;
+};
+
+int fmv_graph_create(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* d_in, double* d_out,
+                     fmv_graph** out) {
+  fmv_graph* g = nullptr;
+  const int rc = guarded([&] {
+    if (!ctx || !op || !d_in || !d_out || !out) fail(FMV_EINVAL, "fmv_graph_create: null argument");
+    if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
+    const auto p = parse_cfg(cfg);
+    DeviceGuard dg(ctx->device);
+    g = new fmv_graph;
+    g->device = ctx->device;
+    g->stream = ctx->stream;
+    const int rc2 = fmv_ctx_create(ctx->device, nullptr, &g->wctx);
+    if (rc2 != FMV_OK) fail(rc2, fmv_last_error());
+    fmv_ctx* w = g->wctx;
+    // warm-up: sizes the workspace, builds twiddle tables, zeroes tickets and
+    // caches kernel attributes, so the captured sequence is kernels only
+    // (a first fp32 / fp16 materialization it triggers stays counted: it happened)
+    g->casts = count_casts(p, false);
+    pipeline(w, op, kind, p, d_in, -1, d_out);
+    CK(cudaStreamSynchronize(w->stream));
+    g_casts.fetch_sub(g->casts, std::memory_order_relaxed);  // the warm-up is not a user matvec
+    CK(cudaStreamBeginCapture(w->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      pipeline(w, op, kind, p, d_in, -1, d_out);
+    } catch (...) {
+      cudaGraph_t dropped = nullptr;
+      cudaStreamEndCapture(w->stream, &dropped);
+      if (dropped) cudaGraphDestroy(dropped);
+      throw;
+    }
+    CK(cudaStreamEndCapture(w->stream, &g->graph));
+    g_casts.fetch_sub(g->casts, std::memory_order_relaxed);  // capture executes nothing
+    CK(cudaGraphInstantiate(&g->exec, g->graph, 0));
+    *out = g;
+  });
+  if (rc != FMV_OK && g) {
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    if (g->wctx) fmv_ctx_destroy(g->wctx);
+    delete g;
+  }
+  return rc;
+}
+
+int fmv_graph_launch(fmv_graph* g) {
+  return guarded([&] {
+    if (!g) fail(FMV_EINVAL, "fmv_graph_launch: null graph");
+    DeviceGuard dg(g->device);
+    CK(cudaGraphLaunch(g->exec, g->stream));
+    g_casts.fetch_add(g->casts, std::memory_order_relaxed);
+  });
+}
+
+int fmv_graph_destroy(fmv_graph* g) {
+  return guarded([&] {
+    if (!g) return;
+    DeviceGuard dg(g->device);
+    cudaStreamSynchronize(g->stream);
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    if (g->wctx) fmv_ctx_destroy(g->wctx);
+    delete g;
+  });
+}
+
 }  // extern "C"

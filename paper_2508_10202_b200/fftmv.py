@@ -33,7 +33,7 @@ __all__ = [
     "setup_operator", "materialize_single", "MatvecKind", "PhaseTimings", "MatvecResult", "phase_name",
     "forward_matvec", "adjoint_matvec", "run_pipeline", "Context", "default_context", "casts_performed",
     "reset_cast_counter", "uniform_fill", "seed_stream", "non_representable_fill", "relative_error", "FmvError",
-    "matvec_block", "forward_matvec_block", "adjoint_matvec_block",
+    "matvec_block", "forward_matvec_block", "adjoint_matvec_block", "MatvecGraph",
 ]
 
 
@@ -496,6 +496,43 @@ def forward_matvec_block(op: SpectralOperator, M, cfg="ddddd"):
 def adjoint_matvec_block(op: SpectralOperator, D, cfg="ddddd"):
     """M = F* D for K sensor vectors (rows of D, each n_d*n_t, SOTI)."""
     return matvec_block(op, MatvecKind.Adjoint, D, cfg)
+
+
+class MatvecGraph:
+    """A device-resident matvec captured once into a CUDA graph
+    (fmv_graph_create) and replayed with one cudaGraphLaunch per call on the
+    context's stream: ``inp`` / ``out`` are CUDA float64 tensors whose
+    contents are read / written at each ``launch()``. For iterative solvers
+    applying F / F* many times to the same buffers."""
+
+    def __init__(self, op: SpectralOperator, kind: MatvecKind, inp, out, cfg="ddddd", ctx: Optional[Context] = None):
+        import torch
+
+        self.ctx = ctx or op.ctx
+        fwd = kind == MatvecKind.Forward
+        n_in = (op.dims.n_m if fwd else op.dims.n_d) * op.dims.n_t
+        n_out = (op.dims.n_d if fwd else op.dims.n_m) * op.dims.n_t
+        for t, n in ((inp, n_in), (out, n_out)):
+            if not _is_cuda_tensor(t) or t.dtype != torch.float64 or t.numel() != n or not t.is_contiguous():
+                raise ValueError("MatvecGraph: inp / out must be contiguous CUDA float64 tensors of the matvec's sizes")
+        self._keep = (op, inp, out)
+        torch.cuda.current_stream(inp.device).synchronize()
+        h = ctypes.c_void_p()
+        check(lib().fmv_graph_create(self.ctx.handle, op.handle, int(kind), _cfg_str(cfg).encode(),
+                                     ctypes.c_void_p(inp.data_ptr()), ctypes.c_void_p(out.data_ptr()), ctypes.byref(h)))
+        self.handle = h
+
+    def launch(self) -> None:
+        check(lib().fmv_graph_launch(self.handle))
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                lib().fmv_graph_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
 
 
 def casts_performed() -> int:
