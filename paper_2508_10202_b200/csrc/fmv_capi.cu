@@ -655,14 +655,15 @@ bool plan_staged(GemvPlan& gp, int mode, size_t es, size_t accsz, int V) {
     // lanes per column: about <= 8 row vectors per lane for short columns,
     // whole warps (or several warps, combined in shared memory) for tall
     // ones; widen when a stage holds too few columns to keep 8 warps busy.
-    // (MV <= 32 -> 2 lanes: fp16 C2 columns, 25 vectors, run 4.9 -> 6.1 TB/s with 2 lanes vs 8)
-    int lpc = MV <= 32 ? 2 : MV <= 128 ? 8 : MV <= 2048 ? 32 : 64;
+    // (fp16 C2 columns, 25 vectors: 4.9 TB/s with 8 lanes, 6.3 with 2, 6.5 with 4)
+    int lpc = MV <= 16 ? 2 : MV <= 32 ? 4 : MV <= 128 ? 8 : MV <= 2048 ? 32 : 64;
     if (lpc > 32) {  // very tall columns: several warps per column
       while (lpc < kConsumers && lpc * 8 < MV) lpc *= 2;
       while ((long)Jc * lpc < kConsumers && lpc < kConsumers) lpc *= 2;
     }
     const int lpc_env = env_int("FMV_SBGEMV_LPC", 0);
-    if (lpc_env == 2 || lpc_env == 8 || lpc_env == 32 || lpc_env == 64 || lpc_env == 128 || lpc_env == 256)
+    if (lpc_env == 2 || lpc_env == 4 || lpc_env == 8 || lpc_env == 32 || lpc_env == 64 || lpc_env == 128 ||
+        lpc_env == 256)
       lpc = lpc_env;
     p.LPC = lpc;
     red = (size_t)(kConsumers / 32) * accsz;
@@ -690,6 +691,7 @@ void sbgemv_staged_v(fmv_ctx* ctx, GemvPlan& gp) {
     else sbgemv_launch_t<MODE, E, O, 4, V, 0>(ctx, gp);
   } else {
     if (gp.p.LPC == 2) sbgemv_launch_t<MODE, E, O, 1, V, 2>(ctx, gp);
+    else if (gp.p.LPC == 4) sbgemv_launch_t<MODE, E, O, 1, V, 4>(ctx, gp);
     else if (gp.p.LPC == 8) sbgemv_launch_t<MODE, E, O, 1, V, 8>(ctx, gp);
     else if (gp.p.LPC == 32) sbgemv_launch_t<MODE, E, O, 1, V, 32>(ctx, gp);
     else sbgemv_launch_t<MODE, E, O, 1, V, 0>(ctx, gp);  // multi-warp columns
