@@ -420,6 +420,9 @@ int fft_lg_series_per_cta(int N, size_t celem) {
 // Register-resident FFT kernels (fmv_fft.cuh k_r2c_reg / k_c2r_reg) cover
 // N = 1000 (10^3) and N = 100 (10^2), SOTI <-> TOSI; everything else (and
 // FMV_FFT_LEGACY=1) uses the general mixed-radix kernels.
+#ifndef FMV_FFT_S64
+#define FMV_FFT_S64 2  // fp64 Nt = 1000 series per CTA of the register FFT kernels
+#endif
 bool fft_reg_ok(int N) {
   return (N == 1000 || N == 100) && env_int("FMV_FFT_LEGACY", 0) == 0;
 }
@@ -435,13 +438,15 @@ void r2c_reg_launch(fmv_ctx* ctx, const Tin* in, long in_ss, long nseries, int n
   else if constexpr (sizeof(Tin) == 4) vec = vec && (reinterpret_cast<uintptr_t>(in) & 7) == 0;
   else vec = false;
   const long grid = (nseries + S - 1) / S;
-  static std::once_flag once;  // static smem only: ask for the max carveout so more CTAs fit per SM
+  constexpr size_t smem = r2c_reg_smem<C, RX, NP, S>();
+  prep_smem((const void*)k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>, smem);
+  static std::once_flag once;  // ask for the max carveout so more CTAs fit per SM
   std::call_once(once, [] {
     CK(cudaFuncSetAttribute((const void*)k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>,
                             cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   });
   launch(ctx, 0, [&] {
-    k_r2c_reg<C0, C1, C2, Tin, RX, NP, S><<<(unsigned)grid, S * RegPlan<RX, NP>::NR, 0, ctx->stream>>>(
+    k_r2c_reg<C0, C1, C2, Tin, RX, NP, S><<<(unsigned)grid, S * RegPlan<RX, NP>::NR, smem, ctx->stream>>>(
         in, in_ss, nseries, nvalid, vec, static_cast<typename PT<C2>::cplx*>(out), out_ks, tw);
   });
 }
@@ -456,7 +461,7 @@ void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, in
     if (in_ts == 1 && out_ss == 1 && fft_reg_ok(N)) {
       constexpr bool f64 = sizeof(R) == 8;
       if (N == 1000)
-        r2c_reg_launch<C0, C1, C2, Tin, 10, 3, f64 ? 2 : 4>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
+        r2c_reg_launch<C0, C1, C2, Tin, 10, 3, f64 ? FMV_FFT_S64 : 4>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
       else
         r2c_reg_launch<C0, C1, C2, Tin, 10, 2, f64 ? 16 : 32>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
       return;
@@ -504,13 +509,16 @@ void c2r_reg_launch(fmv_ctx* ctx, const void* in, long in_ks, long nseries, int 
   const bool vec = sizeof(Tout) == 8 && (out_ss % 2 == 0) && (nout % 2 == 0) &&
                    (reinterpret_cast<uintptr_t>(out) & 15) == 0;
   const long grid = (nseries + S - 1) / S;
+  using Cr = typename CT<typename PT<C3>::real>::c;
+  constexpr size_t smem = c2r_reg_smem<Cr, RX, NP, S>();
+  prep_smem((const void*)k_c2r_reg<C3, C4, Tout, RX, NP, S>, smem);
   static std::once_flag once;
   std::call_once(once, [] {
     CK(cudaFuncSetAttribute((const void*)k_c2r_reg<C3, C4, Tout, RX, NP, S>,
                             cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   });
   launch(ctx, 3, [&] {
-    k_c2r_reg<C3, C4, Tout, RX, NP, S><<<(unsigned)grid, S * RegPlan<RX, NP>::NR, 0, ctx->stream>>>(
+    k_c2r_reg<C3, C4, Tout, RX, NP, S><<<(unsigned)grid, S * RegPlan<RX, NP>::NR, smem, ctx->stream>>>(
         static_cast<const C*>(in), in_ks, nseries, nout, vec, out, out_ss, tw);
   });
 }
@@ -522,7 +530,7 @@ void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, i
   if (in_ss == 1 && fft_reg_ok(N)) {
     constexpr bool f64 = C3 == PD;
     if (N == 1000)
-      c2r_reg_launch<C3, C4, Tout, 10, 3, f64 ? 2 : 4>(ctx, in, in_ks, nseries, nout, out, out_ss);
+      c2r_reg_launch<C3, C4, Tout, 10, 3, f64 ? FMV_FFT_S64 : 4>(ctx, in, in_ks, nseries, nout, out, out_ss);
     else
       c2r_reg_launch<C3, C4, Tout, 10, 2, f64 ? 16 : 32>(ctx, in, in_ks, nseries, nout, out, out_ss);
     return;

@@ -623,6 +623,16 @@ __device__ __forceinline__ void reg_pass(typename CT<R>::c* __restrict__ buf, in
   __syncthreads();
 }
 
+// Dynamic shared-memory bytes of the register kernels (host launch sizes).
+template <class C, int RX, int NP, int S>
+constexpr size_t r2c_reg_smem() {
+  return (size_t)S * reg_series_stride<C, pidx<RX>(RegPlan<RX, NP>::N - 1) + 1, S>() * sizeof(C);
+}
+template <class C, int RX, int NP, int S>
+constexpr size_t c2r_reg_smem() {
+  return (size_t)S * reg_series_stride<C, pidx<RX>(RegPlan<RX, NP>::N) + 1, S>() * sizeof(C);
+}
+
 template <int I, int RX>
 struct IPow {
   static constexpr int v = RX * IPow<I - 1, RX>::v;
@@ -644,7 +654,8 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::
   using OutC = typename PT<C2>::cplx;
   constexpr int N = RegPlan<RX, NP>::N, NR = RegPlan<RX, NP>::NR, T = S * NR;
   constexpr int SS = reg_series_stride<C, pidx<RX>(N - 1) + 1, S>();
-  __shared__ __align__(16) C sbuf[S * SS];
+  extern __shared__ __align__(16) unsigned char reg_smem[];  // S * SS complex (dynamic: S*SS may exceed 48 KB)
+  C* sbuf = reinterpret_cast<C*>(reg_smem);
   const int s = threadIdx.x / NR, j = threadIdx.x - s * NR;
   const long s0 = (long)blockIdx.x * S;
   const int ns = (int)min((long)S, nseries - s0);
@@ -719,7 +730,8 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::
   using C = typename CT<R>::c;
   constexpr int N = RegPlan<RX, NP>::N, NR = RegPlan<RX, NP>::NR, T = S * NR;
   constexpr int SS = reg_series_stride<C, pidx<RX>(N) + 1, S>();
-  __shared__ __align__(16) C sbuf[S * SS];
+  extern __shared__ __align__(16) unsigned char reg_smem[];  // S * SS complex (dynamic: S*SS may exceed 48 KB)
+  C* sbuf = reinterpret_cast<C*>(reg_smem);
   const int s = threadIdx.x / NR, j = threadIdx.x - s * NR;
   const long s0 = (long)blockIdx.x * S;
   const int ns = (int)min((long)S, nseries - s0);
