@@ -577,13 +577,6 @@ __device__ __forceinline__ typename CT<R>::c half_turn10(int q) {
   return {cs[q], -sn[q]};
 }
 
-// Shared-memory position of logical element i (identity: a pad-every-RX
-// layout was measured to trade write conflicts for more read conflicts).
-template <int RX>
-__host__ __device__ constexpr int pidx(int i) {
-  return i;
-}
-
 // Pass-1 store o[q] = v[q], q < RX, for thread j at o = buf + j*RX. With
 // 16-byte elements and even RX, lanes t and t+4 of a quarter-warp would hit
 // the same bank group for every q; lanes with (t>>2)&1 store the pair q^1
@@ -610,7 +603,7 @@ __device__ __forceinline__ void reg_pass(typename CT<R>::c* __restrict__ buf, in
   const int k = j % Ns;
   if (act) {
 #pragma unroll
-    for (int q = 0; q < RX; ++q) v[q] = buf[pidx<RX>(j + q * NR)];
+    for (int q = 0; q < RX; ++q) v[q] = buf[j + q * NR];
     apply_twiddles<R, D, RX, Ns>(v, twp, k);
     butterfly<R, D, RX>(v);
   }
@@ -618,7 +611,7 @@ __device__ __forceinline__ void reg_pass(typename CT<R>::c* __restrict__ buf, in
   if (act) {
     const int o = (j - k) * RX + k;
 #pragma unroll
-    for (int q = 0; q < RX; ++q) buf[pidx<RX>(o + q * Ns)] = v[q];
+    for (int q = 0; q < RX; ++q) buf[o + q * Ns] = v[q];
   }
   __syncthreads();
 }
@@ -626,11 +619,11 @@ __device__ __forceinline__ void reg_pass(typename CT<R>::c* __restrict__ buf, in
 // Dynamic shared-memory bytes of the register kernels (host launch sizes).
 template <class C, int RX, int NP, int S>
 constexpr size_t r2c_reg_smem() {
-  return (size_t)S * reg_series_stride<C, pidx<RX>(RegPlan<RX, NP>::N - 1) + 1, S>() * sizeof(C);
+  return (size_t)S * reg_series_stride<C, RegPlan<RX, NP>::N, S>() * sizeof(C);
 }
 template <class C, int RX, int NP, int S>
 constexpr size_t c2r_reg_smem() {
-  return (size_t)S * reg_series_stride<C, pidx<RX>(RegPlan<RX, NP>::N) + 1, S>() * sizeof(C);
+  return (size_t)S * reg_series_stride<C, RegPlan<RX, NP>::N + 1, S>() * sizeof(C);
 }
 
 template <int I, int RX>
@@ -653,7 +646,7 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::
   using C = typename CT<R>::c;
   using OutC = typename PT<C2>::cplx;
   constexpr int N = RegPlan<RX, NP>::N, NR = RegPlan<RX, NP>::NR, T = S * NR;
-  constexpr int SS = reg_series_stride<C, pidx<RX>(N - 1) + 1, S>();
+  constexpr int SS = reg_series_stride<C, N, S>();
   extern __shared__ __align__(16) unsigned char reg_smem[];  // S * SS complex (dynamic: S*SS may exceed 48 KB)
   C* sbuf = reinterpret_cast<C*>(reg_smem);
   const int s = threadIdx.x / NR, j = threadIdx.x - s * NR;
@@ -713,8 +706,8 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::
     if (si >= ns) continue;
     const C* Z = sbuf + si * SS;
     const int kp = k == 0 ? N : N - k;
-    const C A1 = Z[pidx<RX>(k)];
-    const C A2 = Z[pidx<RX>(k == 0 ? 0 : N - k)];
+    const C A1 = Z[k];
+    const C A2 = Z[k == 0 ? 0 : N - k];
     out[(long)k * out_ks + s0 + si] = cfrom_d<OutC>(to_cd(post(A1, cconj(A2), k)));
     if (kp != k) out[(long)kp * out_ks + s0 + si] = cfrom_d<OutC>(to_cd(post(A2, cconj(A1), kp)));
   }
@@ -729,7 +722,7 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::
   using R = typename PT<C3>::real;
   using C = typename CT<R>::c;
   constexpr int N = RegPlan<RX, NP>::N, NR = RegPlan<RX, NP>::NR, T = S * NR;
-  constexpr int SS = reg_series_stride<C, pidx<RX>(N) + 1, S>();
+  constexpr int SS = reg_series_stride<C, N + 1, S>();
   extern __shared__ __align__(16) unsigned char reg_smem[];  // S * SS complex (dynamic: S*SS may exceed 48 KB)
   C* sbuf = reinterpret_cast<C*>(reg_smem);
   const int s = threadIdx.x / NR, j = threadIdx.x - s * NR;
@@ -759,7 +752,7 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::
 #pragma unroll
       for (int q = 0; q < RX; ++q) {
         const int n = j + q * NR;
-        C A = buf[pidx<RX>(n)], B = buf[pidx<RX>(N - n)];  // X[n], X[N-n]
+        C A = buf[n], B = buf[N - n];  // X[n], X[N-n]
         A.x = A.x * inv_len;
         A.y = n == 0 ? R(0) : A.y * inv_len;  // Im(X0) = 0
         B.x = B.x * inv_len;
@@ -783,7 +776,7 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::
     C v[RX];
     if (act) {
 #pragma unroll
-      for (int q = 0; q < RX; ++q) v[q] = buf[pidx<RX>(j + q * NR)];
+      for (int q = 0; q < RX; ++q) v[q] = buf[j + q * NR];
       apply_twiddles<R, 1, RX, Ns>(v, twp, j);
       butterfly<R, 1, RX>(v);
       Tout* p = out + (s0 + s) * out_ss;
