@@ -530,7 +530,13 @@ void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, i
   if (in_ss == 1 && fft_reg_ok(N)) {
     constexpr bool f64 = C3 == PD;
     if (N == 1000)
-      c2r_reg_launch<C3, C4, Tout, 10, 3, f64 ? FMV_FFT_S64 : 4>(ctx, in, in_ks, nseries, nout, out, out_ss);
+    {
+      // fp32: 8 series per CTA for the big (Nm-series) transform, 2 for the small
+      // one (tools/tune_fft.py at C2: 45.5 -> 39.3 us, and 10.5 us)
+      if constexpr (f64) c2r_reg_launch<C3, C4, Tout, 10, 3, FMV_FFT_S64>(ctx, in, in_ks, nseries, nout, out, out_ss);
+      else if (nseries >= 1024) c2r_reg_launch<C3, C4, Tout, 10, 3, 8>(ctx, in, in_ks, nseries, nout, out, out_ss);
+      else c2r_reg_launch<C3, C4, Tout, 10, 3, 2>(ctx, in, in_ks, nseries, nout, out, out_ss);
+    }
     else
       c2r_reg_launch<C3, C4, Tout, 10, 2, f64 ? 16 : 32>(ctx, in, in_ks, nseries, nout, out, out_ss);
     return;
