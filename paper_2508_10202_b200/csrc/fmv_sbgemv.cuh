@@ -456,19 +456,22 @@ __global__ void __launch_bounds__(FMV_SBGEMV_CONS + 32, FMV_SBGEMV_MINB) k_sbgem
             part[q][v] = kComp ? Tr::zero() : acc[q][v];
             part2[q][v] = Tr::zero();
           }
+        // Pointers stepped per iteration (the thread's row offset folded in
+        // once), so the loop body is loads + MACs + two pointer adds.
         const int G = p.G;
+        const long cstep = (long)G * p.lda;  // elements between this thread's consecutive columns
+        const E* colp = As + (long)g * p.lda + r * V;
+        const E* xp = Xs + g;
         int jj = g;
         constexpr bool kTwo = RPT * V <= 4;  // register budget (wide RPT*V variants keep one chain)
-        if constexpr (kTwo) for (; jj + G < cnt; jj += 2 * G) {
-          const E xv0 = Xs[jj], xv1 = Xs[jj + G];
-          const E* col0 = As + (long)jj * p.lda;
-          const E* col1 = col0 + (long)G * p.lda;
+        if constexpr (kTwo) for (; jj + G < cnt; jj += 2 * G, colp += 2 * cstep, xp += 2 * G) {
+          const E xv0 = xp[0], xv1 = xp[G];
 #pragma unroll
           for (int q = 0; q < RPT; ++q) {
             const int vi = r + q * p.RT;
-            if (vi < MV) {
-              const VecT<E, V> a0 = ldv<E, V>(col0 + vi * V);
-              const VecT<E, V> a1 = ldv<E, V>(col1 + vi * V);
+            if (RPT == 1 || vi < MV) {  // RPT == 1: RT == MV, so every active row is in range
+              const VecT<E, V> a0 = ldv<E, V>(colp + q * p.RT * V);
+              const VecT<E, V> a1 = ldv<E, V>(colp + cstep + q * p.RT * V);
 #pragma unroll
               for (int v = 0; v < V; ++v) {
                 part[q][v] = Tr::mac(part[q][v], a0.e[v], xv0);
@@ -477,14 +480,13 @@ __global__ void __launch_bounds__(FMV_SBGEMV_CONS + 32, FMV_SBGEMV_MINB) k_sbgem
             }
           }
         }
-        for (; jj < cnt; jj += G) {
-          const E xv = Xs[jj];
-          const E* col = As + (long)jj * p.lda;
+        for (; jj < cnt; jj += G, colp += cstep, xp += G) {
+          const E xv = xp[0];
 #pragma unroll
           for (int q = 0; q < RPT; ++q) {
             const int vi = r + q * p.RT;
-            if (vi < MV) {
-              const VecT<E, V> a = ldv<E, V>(col + vi * V);
+            if (RPT == 1 || vi < MV) {
+              const VecT<E, V> a = ldv<E, V>(colp + q * p.RT * V);
 #pragma unroll
               for (int v = 0; v < V; ++v) part[q][v] = Tr::mac(part[q][v], a.e[v], xv);
             }
