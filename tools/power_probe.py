@@ -1,0 +1,37 @@
+"""SBGEMV-N time in three contexts: back-to-back GEMV only, inside the F matvec, and interleaved with an
+fp64 matmul (does the surrounding compute load -- power / clocks -- slow the memory-bound kernel?)."""
+import os, sys, ctypes
+sys.path.insert(0, os.getcwd())
+import torch
+import paper_2508_10202_b200 as F
+from paper_2508_10202_b200 import _capi
+NM, ND, NT = 5000, 100, 1000
+ctx = F.Context(0); L = F.lib()
+st = torch.cuda.ExternalStream(ctx.stream_ptr)
+op = F.setup_operator(F.BlockColumn(F.ProblemDims(NM, ND, NT), F.uniform_fill(NM * ND * NT, 1)), ctx)
+m = torch.from_numpy(F.uniform_fill(NM * NT, 2)).cuda(); yo = torch.empty(ND * NT, dtype=torch.float64, device="cuda")
+A = torch.randn(100 * 5000 * 1001 + 8, dtype=torch.complex128, device="cuda")
+x = torch.randn(5000 * 1001 + 8, dtype=torch.complex128, device="cuda"); y = torch.empty(100 * 1001, dtype=torch.complex128, device="cuda")
+gemv = lambda: _capi.check(L.fmv_sbgemv(ctx.handle, 0, b"z", 100, 5000, 1001, 100, 500000, ctypes.c_void_p(A.data_ptr()), 5000, ctypes.c_void_p(x.data_ptr()), 100, ctypes.c_void_p(y.data_ptr()), 0, None))
+fwd = lambda: _capi.check(L.fmv_matvec_async(ctx.handle, op.handle, 0, b"ddddd", ctypes.c_void_p(m.data_ptr()), ctypes.c_void_p(yo.data_ptr())))
+big = torch.randn(2048, 2048, dtype=torch.float64, device="cuda")
+def fp64_burn():
+    with torch.cuda.stream(st):
+        for _ in range(2): big @ big
+dirty = torch.empty(10 * 2 ** 20, dtype=torch.float64, device="cuda")  # 80 MB, like r2c's TOSI output
+def l2_dirty():
+    with torch.cuda.stream(st):
+        dirty.fill_(1.0)
+small = torch.empty(2 ** 16, dtype=torch.float64, device="cuda")
+def tiny():
+    with torch.cuda.stream(st):
+        small.fill_(1.0)
+for name, seq in (("gemv only", [gemv]), ("F matvec", [fwd]), ("gemv + fp64 matmul", [gemv, fp64_burn]),
+                  ("80 MB write + gemv", [l2_dirty, gemv]), ("tiny kernel + gemv", [tiny, gemv])):
+    for _ in range(3):
+        for f in seq: f()
+    ctx.synchronize(); ctx.set_profiling(True); ctx.profile_read(True)
+    for _ in range(10):
+        for f in seq: f()
+    ms, n = ctx.profile_read(True); ctx.set_profiling(False)
+    print(f"{name:20s}: SBGEMV-N {ms[1] / n[1] * 1e3:7.1f} us ({8.0897e9 / (ms[1] / n[1] * 1e-3) / 1e9:.0f} GB/s)", flush=True)
