@@ -148,7 +148,9 @@ int fmv_sbgemv(fmv_ctx* ctx, int mode, char dtype, size_t m, size_t n, size_t ba
 
 /* ---- 1 x p partition over NCCL (partition.hpp:23-217) ---- */
 int fmv_comm_unique_id(void* out128);
-/* id128: the bytes from rank 0's fmv_comm_unique_id (exchange them out of band). */
+/* id128: the bytes from rank 0's fmv_comm_unique_id (exchange them out of band).
+ * nranks == 1 with id128 == NULL needs no NCCL at all; with an id it builds a
+ * real 1-rank communicator, so the collectives execute (useful for testing). */
 int fmv_comm_init(fmv_ctx* ctx, int nranks, int rank, const void* id128);
 int fmv_comm_destroy(fmv_ctx* ctx);
 /* Each rank holds the operator shard of its Grid1xP column range.
