@@ -100,11 +100,11 @@ int fmv_matvec_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, 
  * nrhs independent inputs back to back (nrhs SOTI vectors of n_in*nt
  * doubles; n_in = nm for FORWARD, nd for ADJOINT), outputs likewise. Each
  * RHS goes through the same 5-phase pipeline and precision config as
- * fmv_matvec; the per-bin SBGEMV handles up to 8 RHS per operator pass
- * (the operator is read from HBM once per 8 RHS instead of once per RHS).
- * Per-RHS results equal fmv_matvec's up to summation order (fp64: ~1e-15
- * relative). 'h' SBGEMV configs and FORWARD with nd > 256 run as nrhs
- * single-RHS pipelines. Blocking; host pointers unless io_on_device. */
+ * fmv_matvec; the per-bin SBGEMV handles up to 8 (FORWARD) / 4 (ADJOINT) RHS
+ * per operator pass (the operator is read from HBM once per pass instead of
+ * once per RHS). Per-RHS results equal fmv_matvec's up to summation order
+ * (fp64: ~1e-15 relative). 'h' SBGEMV configs and FORWARD with nd > 512 run
+ * as nrhs single-RHS pipelines. Blocking; host pointers unless io_on_device. */
 int fmv_matvec_block(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, size_t nrhs, const double* in,
                      double* out, int io_on_device);
 /* Non-blocking variant: device pointers only, enqueued on the ctx stream. */
