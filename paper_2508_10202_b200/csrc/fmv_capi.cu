@@ -19,6 +19,7 @@
 #include <stdexcept>
 #include <string>
 #include <tuple>
+#include <utility>
 #include <vector>
 
 #include "../../include/fftmv_cuda.h"
@@ -406,6 +407,23 @@ void launch(fmv_ctx* ctx, int cls, Fn&& fn) {
   }
 }
 
+// Launch with programmatic dependent launch allowed (FMV_PDL=0 disables).
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  static const bool on = env_int("FMV_PDL", 1) != 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = on ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
 // log2 of the series per CTA (a power of two, <= 16) for a 64 KB smem budget.
 int fft_lg_series_per_cta(int N, size_t celem) {
   const size_t per = 2 * (size_t)(N + 1) * celem;
@@ -446,8 +464,8 @@ void r2c_reg_launch(fmv_ctx* ctx, const Tin* in, long in_ss, long nseries, int n
                             cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   });
   launch(ctx, 0, [&] {
-    k_r2c_reg<C0, C1, C2, Tin, RX, NP, S><<<(unsigned)grid, S * RegPlan<RX, NP>::NR, smem, ctx->stream>>>(
-        in, in_ss, nseries, nvalid, vec, static_cast<typename PT<C2>::cplx*>(out), out_ks, tw);
+    launch_pdl(k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>, dim3((unsigned)grid), dim3(S * RegPlan<RX, NP>::NR), smem,
+               ctx->stream, in, in_ss, nseries, nvalid, vec, static_cast<typename PT<C2>::cplx*>(out), out_ks, tw);
   });
 }
 
@@ -518,8 +536,8 @@ void c2r_reg_launch(fmv_ctx* ctx, const void* in, long in_ks, long nseries, int 
                             cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   });
   launch(ctx, 3, [&] {
-    k_c2r_reg<C3, C4, Tout, RX, NP, S><<<(unsigned)grid, S * RegPlan<RX, NP>::NR, smem, ctx->stream>>>(
-        static_cast<const C*>(in), in_ks, nseries, nout, vec, out, out_ss, tw);
+    launch_pdl(k_c2r_reg<C3, C4, Tout, RX, NP, S>, dim3((unsigned)grid), dim3(S * RegPlan<RX, NP>::NR), smem,
+               ctx->stream, static_cast<const C*>(in), in_ks, nseries, nout, vec, out, out_ss, tw);
   });
 }
 
@@ -605,7 +623,7 @@ void sbgemv_launch_t(fmv_ctx* ctx, GemvPlan& gp) {
     gp.p.partials = ctx->partials.p;
     gp.p.counters = ctx->tickets((size_t)gp.p.batch);
   }
-  launch(ctx, MODE == GM_N ? 1 : 2, [&] { kern<<<(unsigned)P, gp.block, gp.smem, ctx->stream>>>(gp.p); });
+  launch(ctx, MODE == GM_N ? 1 : 2, [&] { launch_pdl(kern, dim3((unsigned)P), dim3(gp.block), gp.smem, ctx->stream, gp.p); });
 }
 
 template <int MODE, class E, class O>

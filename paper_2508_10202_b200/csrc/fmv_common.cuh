@@ -128,4 +128,11 @@ __device__ __forceinline__ C cmuli(C a) {
   else return {a.y, -a.x};
 }
 
+// Programmatic dependent launch: the hot kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so their CTAs may start
+// while the previous kernel drains; griddepcontrol.wait (a no-op for a normal
+// launch) blocks until that kernel's memory operations are visible. Every
+// kernel calls it before its first global access.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace fmv

@@ -654,6 +654,7 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::
   const int ns = (int)min((long)S, nseries - s0);
   const bool act = s < ns;
   C* buf = sbuf + s * SS;
+  grid_dep_wait();  // (PDL)
 
   // Pass 1 (Ns = 1, no twiddles): z[n] = v[2n] + i v[2n+1], n = j + q*NR.
   {
@@ -730,6 +731,7 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::
   const int ns = (int)min((long)S, nseries - s0);
   const bool act = s < ns;
   C* buf = sbuf + s * SS;
+  grid_dep_wait();  // (PDL)
   const R inv_len = R(1) / (R)(2 * N);
 
   // The N+1 bins of S series (bin-major runs of S in global memory) land in

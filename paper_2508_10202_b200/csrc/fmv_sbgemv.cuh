@@ -377,6 +377,7 @@ __global__ void __launch_bounds__(FMV_SBGEMV_CONS + 32, FMV_SBGEMV_MINB) k_sbgem
     }
     mbar_fence_init();
   }
+  grid_dep_wait();  // (PDL) the previous kernel's x / y writes are visible from here on
   __syncthreads();
 
   const long c0 = p.T * (long)blockIdx.x / p.P;
