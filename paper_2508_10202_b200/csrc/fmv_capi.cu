@@ -478,7 +478,10 @@ void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, in
   if constexpr (tin_ok) {
     if (in_ts == 1 && out_ss == 1 && fft_reg_ok(N)) {
       constexpr bool f64 = sizeof(R) == 8;
-      if (N == 1000)
+      // (fp64: one series per CTA for small batches -- more CTAs for the 100-series transforms)
+      if (N == 1000 && f64 && nseries < 1024)
+        r2c_reg_launch<C0, C1, C2, Tin, 10, 3, 1>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
+      else if (N == 1000)
         r2c_reg_launch<C0, C1, C2, Tin, 10, 3, f64 ? FMV_FFT_S64 : 4>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
       else
         r2c_reg_launch<C0, C1, C2, Tin, 10, 2, f64 ? 16 : 32>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
@@ -551,7 +554,10 @@ void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, i
     {
       // fp32: 8 series per CTA for the big (Nm-series) transform, 2 for the small
       // one (tools/tune_fft.py at C2: 45.5 -> 39.3 us, and 10.5 us)
-      if constexpr (f64) c2r_reg_launch<C3, C4, Tout, 10, 3, FMV_FFT_S64>(ctx, in, in_ks, nseries, nout, out, out_ss);
+      if constexpr (f64) {
+        if (nseries < 1024) c2r_reg_launch<C3, C4, Tout, 10, 3, 1>(ctx, in, in_ks, nseries, nout, out, out_ss);
+        else c2r_reg_launch<C3, C4, Tout, 10, 3, FMV_FFT_S64>(ctx, in, in_ks, nseries, nout, out, out_ss);
+      }
       else if (nseries >= 1024) c2r_reg_launch<C3, C4, Tout, 10, 3, 8>(ctx, in, in_ks, nseries, nout, out, out_ss);
       else c2r_reg_launch<C3, C4, Tout, 10, 3, 2>(ctx, in, in_ks, nseries, nout, out, out_ss);
     }
