@@ -23,11 +23,19 @@ def l2_dirty():
     with torch.cuda.stream(st):
         dirty.fill_(1.0)
 small = torch.empty(2 ** 16, dtype=torch.float64, device="cuda")
+sink = torch.empty(1, dtype=torch.float64, device="cuda")
+def l2_read():  # read 80 MB (clean lines), no writes
+    with torch.cuda.stream(st):
+        sink.copy_(dirty.sum().reshape(1))
+def write8():  # 8 MB write
+    with torch.cuda.stream(st):
+        dirty[: 2 ** 20].fill_(2.0)
 def tiny():
     with torch.cuda.stream(st):
         small.fill_(1.0)
 for name, seq in (("gemv only", [gemv]), ("F matvec", [fwd]), ("gemv + fp64 matmul", [gemv, fp64_burn]),
-                  ("80 MB write + gemv", [l2_dirty, gemv]), ("tiny kernel + gemv", [tiny, gemv])):
+                  ("80 MB write + gemv", [l2_dirty, gemv]), ("tiny kernel + gemv", [tiny, gemv]),
+                  ("80 MB read + gemv", [l2_read, gemv]), ("8 MB write + gemv", [write8, gemv])):
     for _ in range(3):
         for f in seq: f()
     ctx.synchronize(); ctx.set_profiling(True); ctx.profile_read(True)
