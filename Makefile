@@ -7,9 +7,11 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr -Xptxas -v
 PKG := paper_2508_10202_b200
+# nlohmann/json.hpp (sweep.hpp includes it unconditionally, as the reference's sweep.hpp:20 does)
+JSON_INC := $(shell python -c "import sysconfig;print(sysconfig.get_paths()['purelib'])")/include/cudnn_frontend/thirdparty/nlohmann
 SRC := $(wildcard $(PKG)/csrc/*.cu) $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.cpp) include/fftmv_cuda.h
 
-all: lib oracle cpp cli
+all: lib oracle cpp cli stub
 
 lib: $(PKG)/libfftmv_cuda.so
 
@@ -23,16 +25,27 @@ cpp: build/fftmv_cpp_tests
 
 build/fftmv_cpp_tests: tests/cpp/test_dropin.cpp $(wildcard include/fftmv/*.hpp) include/fftmv_cuda.h $(PKG)/libfftmv_cuda.so
 	@mkdir -p build
-	g++ -std=c++20 -O2 -Wall -Iinclude -I/usr/local/cuda/include -I$(shell python -c "import sysconfig;print(sysconfig.get_paths()['purelib'])")/include/cudnn_frontend/thirdparty/nlohmann -o $@ tests/cpp/test_dropin.cpp -L$(PKG) -lfftmv_cuda -Wl,-rpath,'$$ORIGIN/../$(PKG)' -L/usr/local/cuda/lib64 -lcudart
+	g++ -std=c++20 -O2 -Wall -Iinclude -I/usr/local/cuda/include -I$(JSON_INC) -o $@ tests/cpp/test_dropin.cpp -L$(PKG) -lfftmv_cuda -Wl,-rpath,'$$ORIGIN/../$(PKG)' -L/usr/local/cuda/lib64 -lcudart
 
-cli: build/fft_matvec
+cli: build/fft_matvec build/fftmv_dropin_bench
+
+build/fftmv_dropin_bench: $(PKG)/cli/dropin_bench.cpp $(wildcard include/fftmv/*.hpp) include/fftmv_cuda.h $(PKG)/libfftmv_cuda.so
+	@mkdir -p build
+	g++ -std=c++20 -O2 -Wall -Iinclude -I/usr/local/cuda/include -o $@ $(PKG)/cli/dropin_bench.cpp -L$(PKG) -lfftmv_cuda -Wl,-rpath,'$$ORIGIN/../$(PKG)' -L/usr/local/cuda/lib64 -lcudart
+
+# test-only NCCL API over POSIX shared memory (FMV_NCCL_LIB): several ranks on one GPU
+stub: build/libfmv_nccl_stub.so
+
+build/libfmv_nccl_stub.so: tests/stub/fmv_nccl_stub.cpp
+	@mkdir -p build
+	g++ -std=c++20 -O2 -Wall -fPIC -shared -I/usr/local/cuda/include -o $@ $< -L/usr/local/cuda/lib64 -lcudart -lrt
 
 build/fft_matvec: $(PKG)/cli/fft_matvec.cpp $(wildcard include/fftmv/*.hpp) include/fftmv_cuda.h $(PKG)/libfftmv_cuda.so
 	@mkdir -p build
-	g++ -std=c++20 -O2 -Wall -Iinclude -I/usr/local/cuda/include -o $@ $(PKG)/cli/fft_matvec.cpp -L$(PKG) -lfftmv_cuda -Wl,-rpath,'$$ORIGIN/../$(PKG)' -L/usr/local/cuda/lib64 -lcudart
+	g++ -std=c++20 -O2 -Wall -Iinclude -I/usr/local/cuda/include -I$(JSON_INC) -o $@ $(PKG)/cli/fft_matvec.cpp -L$(PKG) -lfftmv_cuda -Wl,-rpath,'$$ORIGIN/../$(PKG)' -L/usr/local/cuda/lib64 -lcudart
 
 clean:
-	rm -f $(PKG)/libfftmv_cuda.so build/fftmv_cpp_tests build/fft_matvec
+	rm -f $(PKG)/libfftmv_cuda.so build/fftmv_cpp_tests build/fft_matvec build/libfmv_nccl_stub.so
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib oracle cpp cli clean
+.PHONY: all lib oracle cpp cli stub clean

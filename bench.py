@@ -34,6 +34,8 @@ import time
 os.environ.setdefault("MKL_NUM_THREADS", "1")
 # NCCL prints its version banner on stdout at init; keep stdout for the one JSON line
 os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator size / transport in the driver's stderr log
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
@@ -152,10 +154,22 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
+def ref_inputs(R):
+    """make_inputs() through the reference's own generators (oracle/_ref:
+    random_fill.hpp compiled verbatim): the same bits, and nothing of this
+    repo's package is loaded in the reference arm."""
+    col = R.uniform_fill(NT * ND * NM, R.seed_stream(SEED, 0))
+    m = R.uniform_fill(NM * NT, R.seed_stream(SEED, 1))
+    d = R.uniform_fill(ND * NT, R.seed_stream(SEED, 2))
+    return col, m, d
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return None
-    col, m, d = make_inputs(0)
+    from oracle.oracle import ref
+
+    col, m, d = ref_inputs(ref())
     R, op, t_setup = ref_setup(col)
     T = cpu_threads()
     cfg = args.cfg
@@ -221,6 +235,9 @@ def run_ours(args, rank, world, local_rank):
     dm = None
     if world > 1 or os.environ.get("FMV_BENCH_FORCE_DIST") == "1":  # (the latter: exercise the NCCL path on 1 GPU)
         dm = F.DistributedMatvec(F.ProblemDims(NM * world, ND, NT), rank, world, shard=op, transport="native", ctx=ctx)
+        nranks, crank = dm.comm_size()
+        if nranks != world or crank != rank:
+            raise SystemExit(f"bench: communicator has {nranks} ranks (this rank {crank}), expected {world} ({rank})")
 
     def step_device():
         if dm is None:
@@ -350,9 +367,31 @@ def run_ours(args, rank, world, local_rank):
     }
     if world == 1 and not args.no_block and cfg[2] in "ds":
         line["block"] = block_throughput(F, L, ctx, op, cfg, m_h, d_h, dev, stream)
+    if rank == 0 and world == 1 and not args.no_dropin:
+        line["e2e_dropin"] = dropin_e2e(cfg, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(col, m_h, d_h, cfg)
     return line
+
+
+def dropin_e2e(cfg, args):
+    """Second end-to-end figure: the reference's own C++ API (include/fftmv
+    forward_matvec / adjoint_matvec with std::vector host vectors and
+    PhaseTimings, build/fftmv_dropin_bench), host wall clock per step, in a
+    separate process on the same GPU."""
+    exe = os.path.join(HERE, "build", "fftmv_dropin_bench")
+    if not os.path.exists(exe):
+        return {"value": None, "unit": UNIT, "note": "build/fftmv_dropin_bench not built (make cli)"}
+    try:
+        r = subprocess.run([exe, str(NM), str(ND), str(NT), cfg, str(args.steps), str(max(3, args.warmup))],
+                           capture_output=True, text=True, timeout=600)
+        j = json.loads(r.stdout.strip().splitlines()[-1])
+        return {"value": j["matvecs_per_s"], "unit": UNIT, "ms_per_step": j["ms_per_step"],
+                "h2d_bytes_per_step": j["h2d_bytes_per_step"], "d2h_bytes_per_step": j["d2h_bytes_per_step"],
+                "api": "C++ drop-in fftmv::forward_matvec / adjoint_matvec (reference signatures, pageable "
+                       "std::vector I/O, PhaseTimings on), host wall clock"}
+    except Exception as e:  # report, do not hide
+        return {"value": None, "unit": UNIT, "note": f"dropin bench failed: {e}"}
 
 
 def block_throughput(F, L, ctx, op, cfg, m_h, d_h, dev, stream, reps=5):
@@ -400,6 +439,26 @@ def cpu_baseline(col, m, d, cfg):
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
 
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` without a launcher: re-exec as N ranks (one
+    per GPU) under torch.distributed.run on 127.0.0.1, as the driver does."""
+    import socket
+
+    import torch
+
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but only {n} visible GPUs")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("NCCL_DEBUG", "INFO")  # to stderr (NCCL_DEBUG_FILE): shows the communicator's nranks
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -409,6 +468,7 @@ def main():
     ap.add_argument("--cfg", default="ddddd")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-block", action="store_true", help="skip the block (multi-RHS) extra measurement")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the C++ drop-in e2e measurement")
     ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
                     help="c2: Nm=5000, Nd=100, Nt=1000 per GPU (default); c5: Nd=600 (48 GB fp64 operator per GPU)")
     args = ap.parse_args()
@@ -418,10 +478,20 @@ def main():
         args.no_cpu_baseline = True  # the reference needs ~70 GB host RAM and minutes of setup at C5
     if args.warmup < 3:
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        relaunch_under_torchrun(args)  # does not return
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
     local_rank = env_int("LOCAL_RANK", 0)
+    if "WORLD_SIZE" in os.environ and args.impl == "ours" and world != args.gpus and "--gpus" in " ".join(sys.argv):
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1 and args.impl == "ours":
+        import torch
+
+        if torch.cuda.device_count() < world:
+            raise SystemExit(f"bench: {world} ranks but only {torch.cuda.device_count()} visible GPUs")
+        if local_rank >= torch.cuda.device_count():
+            raise SystemExit(f"bench: LOCAL_RANK {local_rank} has no GPU")
         import torch
         import torch.distributed as dist
 

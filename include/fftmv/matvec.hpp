@@ -2,8 +2,10 @@
 // (matvec.hpp:40-318). The whole pipeline runs in three fused sm_100a
 // kernels inside libfftmv_cuda (fmv_matvec): pad+cast+r2c+reorder,
 // SBGEMV (+ both reorders and casts), reorder+1/L+c2r+unpad+cast.
-// PhaseTimings attribution on B200: [0] H2D of the input, [1] r2c kernel,
-// [2] SBGEMV kernel, [3] c2r kernel, [4] D2H of the output.
+// PhaseTimings attribution on B200 (fftmv_cuda.h): [0] H2D of the input,
+// [1] r2c kernels, [2] SBGEMV kernels, [3] c2r kernels, [4] D2H of the
+// output, each the summed CUDA-event time; the host copies overlap the
+// SBGEMV column chunks, so the phases may sum to more than total_s.
 #pragma once
 
 #include <array>
@@ -67,19 +69,28 @@ inline std::pair<std::vector<double>, PhaseTimings> run_pipeline(const SpectralO
   const bool fwd = kind == MatvecKind::Forward;
   const std::size_t n_in = (fwd ? op.dims.n_m : op.dims.n_d) * op.dims.n_t;
   const std::size_t n_out = (fwd ? op.dims.n_d : op.dims.n_m) * op.dims.n_t;
-  std::vector<double> staged;
-  std::string c = cfg.render();
-  if (payload) {
-    // payload already rounded to cfg[0] (partition.hpp:196-206): pad it as is
-    staged = payload->prec == Precision::Double ? payload->d : std::vector<double>(payload->f.begin(), payload->f.end());
-    input = staged;
-    c[0] = 'd';
-  }
-  if (input.size() != n_in) throw std::invalid_argument("matvec: input length does not match operator dims");
+  const std::string c = cfg.render();
   std::vector<double> out(n_out);
   fmv_phase_times t{};
-  check(fmv_matvec(thread_ctx(), op.handle(), fwd ? FMV_FORWARD : FMV_ADJOINT, c.c_str(), input.data(), out.data(), 0,
-                   &t));
+  fmv_ctx* ctx = thread_ctx(op.device());
+  const int k = fwd ? FMV_FORWARD : FMV_ADJOINT;
+  if (payload) {
+    // payload already rounded to cfg[0] (partition.hpp:196-206): phase 1 pads
+    // it as is, in its own precision
+    if (payload->size() != n_in) throw std::invalid_argument("matvec: input length does not match operator dims");
+    if (payload->prec == Precision::Double) {
+      check(fmv_matvec_payload(ctx, op.handle(), k, c.c_str(), 'd', payload->d.data(), out.data(), 0, &t));
+    } else if (payload->prec == Precision::Single) {
+      check(fmv_matvec_payload(ctx, op.handle(), k, c.c_str(), 's', payload->f.data(), out.data(), 0, &t));
+    } else {  // fp16 extension: the float buffer holds binary16 values exactly
+      std::vector<_Float16> h(payload->f.size());
+      for (std::size_t i = 0; i < h.size(); ++i) h[i] = static_cast<_Float16>(payload->f[i]);
+      check(fmv_matvec_payload(ctx, op.handle(), k, c.c_str(), 'h', h.data(), out.data(), 0, &t));
+    }
+  } else {
+    if (input.size() != n_in) throw std::invalid_argument("matvec: input length does not match operator dims");
+    check(fmv_matvec(ctx, op.handle(), k, c.c_str(), input.data(), out.data(), 0, &t));
+  }
   PhaseTimings pt;
   for (int i = 0; i < 5; ++i) pt.phase_s[i] = t.phase_s[i];
   pt.total_s = t.total_s;
@@ -129,7 +140,7 @@ inline std::vector<BlockVector> matvec_block(const SpectralOperator& op, const s
   }
   std::vector<double> out(in.size() * n_out);
   if (!in.empty())
-    check(fmv_matvec_block(thread_ctx(), op.handle(), fwd ? FMV_FORWARD : FMV_ADJOINT, cfg.render().c_str(),
+    check(fmv_matvec_block(thread_ctx(op.device()), op.handle(), fwd ? FMV_FORWARD : FMV_ADJOINT, cfg.render().c_str(),
                            in.size(), packed.data(), out.data(), 0));
   std::vector<BlockVector> res;
   res.reserve(in.size());

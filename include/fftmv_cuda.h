@@ -50,9 +50,15 @@ typedef struct fmv_op fmv_op;
 
 /* PhaseTimings (matvec.hpp:42-51): seconds per phase + total. On B200 the
  * phases are fused, so: [0] host->device copy of the input (0 when the I/O is
- * device-resident), [1] pad+cast+r2c kernel, [2] SBGEMV kernel incl. both
- * fused reorders, [3] c2r+unpad kernel, [4] device->host copy (+ reduce for
- * the partitioned forward). */
+ * device-resident; + payload cast and broadcast for the partitioned
+ * adjoint, partition.hpp:204-206), [1] pad+cast+r2c kernels, [2] SBGEMV
+ * kernels incl. both fused reorders, [3] c2r+unpad kernels, [4]
+ * device->host copy (+ the reduce of the partitioned forward,
+ * partition.hpp:178-180). Each phase is the summed CUDA-event time of its
+ * kernels / copies. Host-I/O calls overlap the copies and the FFTs with the
+ * SBGEMV (column chunks), so the phases may add up to more than total_s,
+ * the wall time of the whole call; requesting times does not change the
+ * schedule. */
 typedef struct {
   double phase_s[5];
   double total_s;
@@ -93,6 +99,13 @@ size_t fmv_op_device_bytes(const fmv_op* op);
  * (pinned or pageable) unless io_on_device. times may be NULL. */
 int fmv_matvec(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* in, double* out,
                int io_on_device, fmv_phase_times* times);
+/* run_pipeline with a broadcast payload (matvec.hpp:233-289 `payload`,
+ * partition.hpp:198-212): `in` holds the input already rounded to cfg[0] in
+ * payload_prec ('d' double, 's' float, 'h' IEEE binary16 bits), so phase 1
+ * pads it without another rounding and the cast counter does not count a pad
+ * cast. Otherwise as fmv_matvec. */
+int fmv_matvec_payload(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, char payload_prec, const void* in,
+                       double* out, int io_on_device, fmv_phase_times* times);
 /* Non-blocking variant: device pointers only, enqueued on the ctx stream. */
 int fmv_matvec_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* d_in, double* d_out);
 
@@ -153,9 +166,19 @@ int fmv_comm_unique_id(void* out128);
  * real 1-rank communicator, so the collectives execute (useful for testing). */
 int fmv_comm_init(fmv_ctx* ctx, int nranks, int rank, const void* id128);
 int fmv_comm_destroy(fmv_ctx* ctx);
+/* The live communicator's size and this rank (1 and 0 without one). */
+int fmv_comm_size(const fmv_ctx* ctx, int* nranks, int* rank);
 /* Each rank holds the operator shard of its Grid1xP column range.
  * FORWARD: in = this rank's m slice (shard_nm*nt), out = full d (nd*nt) on
- *   every rank, partial d summed in cfg[4] precision (partition.hpp:157-182).
+ *   every rank, partial d summed in cfg[4] precision (partition.hpp:157-182)
+ *   with the reference's fixed left-balanced tree over the all-gathered
+ *   partials (tree_reduce, partition.hpp:84-107): bitwise the in-process
+ *   result for every p.
+ * Collectives are watched: an asynchronous NCCL error, or no completion
+ *   within FMV_NCCL_TIMEOUT_S seconds (default 600), aborts the
+ *   communicator and returns FMV_ENCCL (re-init before the next call).
+ * FMV_NCCL_LIB (environment) loads another library with the NCCL API in
+ *   place of libnccl.so.2.
  * ADJOINT: in = full d (nd*nt, read on rank 0 only), broadcast in cfg[0]
  *   precision; out = this rank's m slice (partition.hpp:187-217). */
 int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* shard, int kind, const char* cfg, const double* in,

@@ -183,6 +183,16 @@ class Ref(_Base):
             raise ValueError(self.err())
         return out, t
 
+    def matvec_many(self, op, jobs, threads=None):
+        """Run [(kind, cfg, x), ...] on a shared operator across host threads
+        (the reference's matvecs are reentrant on one operator, SPEC.md:291;
+        ctypes drops the GIL for the call). Returns the outputs in job order."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        threads = threads or min(len(jobs), len(os.sched_getaffinity(0)))
+        with ThreadPoolExecutor(max_workers=max(1, threads)) as ex:
+            return list(ex.map(lambda j: self.matvec(op, j[0], j[1], j[2]), jobs))
+
     def throughput(self, op, kind, cfg, x, threads, per_thread):
         x = np.ascontiguousarray(x, dtype=np.float64)
         s = c_double()

@@ -56,6 +56,8 @@ def lib() -> ctypes.CDLL:
         "fmv_op_download_bins": (c_int, [c_void_p, c_void_p, c_char, c_void_p]),
         "fmv_op_device_bytes": (c_size_t, [c_void_p]),
         "fmv_matvec": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_void_p, c_void_p, c_int, POINTER(PhaseTimesC)]),
+        "fmv_matvec_payload": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_char, c_void_p, c_void_p, c_int,
+                                       POINTER(PhaseTimesC)]),
         "fmv_matvec_async": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_void_p, c_void_p]),
         "fmv_matvec_block": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_size_t, c_void_p, c_void_p, c_int]),
         "fmv_matvec_block_async": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_size_t, c_void_p, c_void_p]),
@@ -66,6 +68,7 @@ def lib() -> ctypes.CDLL:
         "fmv_comm_unique_id": (c_int, [c_void_p]),
         "fmv_comm_init": (c_int, [c_void_p, c_int, c_int, c_void_p]),
         "fmv_comm_destroy": (c_int, [c_void_p]),
+        "fmv_comm_size": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int)]),
         "fmv_matvec_partitioned": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_void_p, c_void_p, c_int,
                                            POINTER(PhaseTimesC)]),
         "fmv_graph_create": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_void_p, c_void_p, POINTER(c_void_p)]),
@@ -97,7 +100,7 @@ def exported_symbols() -> list[str]:
         "fmv_comm_unique_id", "fmv_comm_init", "fmv_comm_destroy", "fmv_matvec_partitioned", "fmv_seed_stream",
         "fmv_uniform_fill", "fmv_non_representable_fill", "fmv_relative_error", "fmv_fft_r2c", "fmv_fft_c2r",
         "fmv_matvec_block", "fmv_matvec_block_async", "fmv_comm_init_2d", "fmv_matvec_partitioned_2d",
-        "fmv_graph_create", "fmv_graph_launch", "fmv_graph_destroy",
+        "fmv_graph_create", "fmv_graph_launch", "fmv_graph_destroy", "fmv_matvec_payload", "fmv_comm_size",
     ]
 
 

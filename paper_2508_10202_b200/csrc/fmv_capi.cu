@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <array>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -18,6 +19,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <utility>
 #include <vector>
@@ -234,15 +236,39 @@ int env_int(const char* name, int dflt) {
   return v && *v ? atoi(v) : dflt;
 }
 
-// Raise a kernel's dynamic shared-memory cap once per (function, size).
+// Kernel attributes are per device (cudaFuncSetAttribute applies to the
+// current one), so both caches are keyed by (device, function).
+int cur_device() {
+  int d = 0;
+  CK(cudaGetDevice(&d));
+  return d;
+}
+
+// Raise a kernel's dynamic shared-memory cap once per (device, function, size).
 void prep_smem(const void* fn, size_t bytes) {
   static std::mutex mu;
-  static std::map<const void*, size_t> set;
+  static std::map<std::pair<int, const void*>, size_t> set;
+  if (bytes <= 48 * 1024) return;
+  const int dev = cur_device();
   std::lock_guard<std::mutex> lk(mu);
-  size_t& cur = set[fn];
-  if (bytes > 48 * 1024 && bytes > cur) {
+  size_t& cur = set[{dev, fn}];
+  if (bytes > cur) {
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     cur = bytes;
+  }
+}
+
+// Ask for the maximum shared-memory carveout once per (device, function), so
+// more CTAs of the register FFT kernels fit per SM.
+void prep_carveout(const void* fn) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, bool> set;
+  const int dev = cur_device();
+  std::lock_guard<std::mutex> lk(mu);
+  bool& done = set[{dev, fn}];
+  if (!done) {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    done = true;
   }
 }
 
@@ -263,39 +289,58 @@ int sm_count(int dev) {
 // ======================================================================
 struct Nccl {
   typedef int (*GetUniqueId)(void*);
-  typedef int (*CommInitRank)(void**, int, char[128], int);  // ncclUniqueId passed by value (128 bytes)
   typedef int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+  typedef int (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t);
   typedef int (*Broadcast)(const void*, void*, size_t, int, int, void*, cudaStream_t);
   typedef int (*CommDestroy)(void*);
+  typedef int (*CommAbort)(void*);
   typedef int (*CommSplit)(void*, int, int, void**, void*);
+  typedef int (*GetAsyncError)(void*, int*);
   typedef const char* (*GetErrorString)(int);
   void* h = nullptr;
+  std::string path;
   GetUniqueId get_unique_id = nullptr;
-  void* comm_init_rank = nullptr;
+  void* comm_init_rank = nullptr;  // ncclUniqueId (128 bytes) is passed by value: cast at the call site
   AllReduce all_reduce = nullptr;
+  AllGather all_gather = nullptr;
   Broadcast broadcast = nullptr;
   CommDestroy comm_destroy = nullptr;
+  CommAbort comm_abort = nullptr;
   CommSplit comm_split = nullptr;
+  GetAsyncError get_async_error = nullptr;
   GetErrorString err = nullptr;
 };
+// NCCL is dlopen'ed on first use (only the partitioned path needs it).
+// FMV_NCCL_LIB names another library exporting the same symbols (e.g. the
+// host-staged test transport, tests/stub/fmv_nccl_stub.cpp, which lets
+// several processes share one GPU).
 Nccl& nccl() {
   static Nccl n;
   static std::once_flag once;
   std::call_once(once, [] {
-    const char* names[] = {"libnccl.so.2", "libnccl.so"};
-    for (const char* nm : names)
-      if ((n.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+    std::vector<std::string> names;
+    if (const char* e = getenv("FMV_NCCL_LIB"); e && *e) names.push_back(e);
+    else names = {"libnccl.so.2", "libnccl.so"};
+    for (const auto& nm : names)
+      if ((n.h = dlopen(nm.c_str(), RTLD_NOW | RTLD_GLOBAL))) {
+        n.path = nm;
+        break;
+      }
     if (!n.h) return;
     n.get_unique_id = (Nccl::GetUniqueId)dlsym(n.h, "ncclGetUniqueId");
     n.comm_init_rank = dlsym(n.h, "ncclCommInitRank");
     n.all_reduce = (Nccl::AllReduce)dlsym(n.h, "ncclAllReduce");
+    n.all_gather = (Nccl::AllGather)dlsym(n.h, "ncclAllGather");
     n.broadcast = (Nccl::Broadcast)dlsym(n.h, "ncclBroadcast");
     n.comm_destroy = (Nccl::CommDestroy)dlsym(n.h, "ncclCommDestroy");
+    n.comm_abort = (Nccl::CommAbort)dlsym(n.h, "ncclCommAbort");
     n.comm_split = (Nccl::CommSplit)dlsym(n.h, "ncclCommSplit");
+    n.get_async_error = (Nccl::GetAsyncError)dlsym(n.h, "ncclCommGetAsyncError");
     n.err = (Nccl::GetErrorString)dlsym(n.h, "ncclGetErrorString");
   });
-  if (!n.h || !n.get_unique_id || !n.comm_init_rank || !n.all_reduce || !n.broadcast)
-    fail(FMV_ENCCL, "NCCL (libnccl.so.2) could not be loaded");
+  if (!n.h || !n.get_unique_id || !n.comm_init_rank || !n.all_gather || !n.broadcast)
+    fail(FMV_ENCCL, std::string("NCCL (") + (getenv("FMV_NCCL_LIB") ? getenv("FMV_NCCL_LIB") : "libnccl.so.2") +
+                        ") could not be loaded: " + (n.h ? "missing symbols" : dlerror() ? dlerror() : "dlopen failed"));
   return n;
 }
 void nck(int rc, const char* what) {
@@ -354,6 +399,15 @@ struct fmv_ctx {
   void* col_comm = nullptr;
   int pr = 1, pc = 1, ri = 0, cj = 0;
   cudaEvent_t te[8] = {};
+  // PhaseTimings of one blocking matvec (fmv_matvec with times != NULL):
+  // every kernel launch, copy and collective records a CUDA-event pair on the
+  // stream it runs on, tagged with the reference phase it belongs to.
+  bool phase_timing = false;
+  struct PhaseRec {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  std::vector<PhaseRec> phase_recs;
 
   cudaEvent_t ev() {
     if (!ev_pool.empty()) {
@@ -380,8 +434,10 @@ struct fmv_op {
   int device = 0;
   size_t nm = 0, nd = 0, nt = 0;
   void* bins_d = nullptr;  // double2, lda = nd
-  void* bins_s = nullptr;  // float2, lda = lda_s
-  void* bins_h = nullptr;  // __half2, lda = lda_h
+  // fp32 / fp16 copies, published (release) only after their cast kernel has
+  // finished and lda_s / lda_h are set; readers load them with acquire.
+  std::atomic<void*> bins_s{nullptr};  // float2, lda = lda_s
+  std::atomic<void*> bins_h{nullptr};  // __half2, lda = lda_h
   size_t lda_s = 0, lda_h = 0;
   std::mutex mu;
   size_t nb() const { return nt + 1; }
@@ -390,22 +446,88 @@ struct fmv_op {
 namespace {
 
 // ---------------------------------------------------------------- launch --
+// Reference phase (matvec.hpp:42-51) a kernel class is charged to: r2c ->
+// [1] fft (pad + convert + reorder fused in), SBGEMV -> [2], c2r -> [3] ifft
+// (reorder + unpad fused in). Class 4 (cast kernels) is charged explicitly by
+// the caller; a first fp32/fp16 operator materialization inside a matvec goes
+// to [2] like the reference's ensure_single inside gemv_stage.
+constexpr int kPhaseOfClass[5] = {1, 2, 2, 3, 2};
+
+// Run fn (which enqueues work on `s`) inside a CUDA-event span of `phase`
+// when the context is collecting PhaseTimings.
 template <class Fn>
-void launch(fmv_ctx* ctx, int cls, Fn&& fn) {
+void phase_span(fmv_ctx* ctx, cudaStream_t s, int phase, Fn&& fn) {
+  if (!ctx->phase_timing) {
+    fn();
+    return;
+  }
+  fmv_ctx::PhaseRec r{phase, ctx->ev(), ctx->ev()};
+  CK(cudaEventRecord(r.a, s));
+  fn();
+  CK(cudaEventRecord(r.b, s));
+  ctx->phase_recs.push_back(r);
+}
+
+template <class Fn>
+void launch(fmv_ctx* ctx, int cls, Fn&& fn, int phase = -1) {
   ProfRec r{cls, nullptr, nullptr};
   if (ctx->profiling) {
     r.a = ctx->ev();
     r.b = ctx->ev();
     CK(cudaEventRecord(r.a, ctx->stream));
   }
-  fn();
-  CK(cudaGetLastError());
+  phase_span(ctx, ctx->stream, phase >= 0 ? phase : kPhaseOfClass[cls], [&] {
+    fn();
+    CK(cudaGetLastError());
+  });
   ++ctx->launches;
   if (ctx->profiling) {
     CK(cudaEventRecord(r.b, ctx->stream));
     ctx->prof.push_back(r);
   }
 }
+
+// cudaMemcpyAsync charged to a phase ([0] for input copies, [4] for output).
+void copy_async(fmv_ctx* ctx, int phase, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+                cudaStream_t s) {
+  phase_span(ctx, s, phase, [&] { CK(cudaMemcpyAsync(dst, src, bytes, kind, s)); });
+}
+
+// Collects the phase spans of one matvec: sums the busy time per phase
+// (spans of one phase never overlap each other; spans of different phases
+// may, on the overlapped host-I/O path) and the wall time from `t0` to `t1`
+// (events recorded on the matvec stream around everything). Call after the
+// stream has been synchronized.
+void collect_phase_times(fmv_ctx* ctx, cudaEvent_t t0, cudaEvent_t t1, fmv_phase_times* out) {
+  double ms[5] = {0, 0, 0, 0, 0};
+  for (auto& r : ctx->phase_recs) {
+    float v = 0.f;
+    CK(cudaEventElapsedTime(&v, r.a, r.b));
+    ms[r.phase] += v;
+    ctx->ev_pool.push_back(r.a);
+    ctx->ev_pool.push_back(r.b);
+  }
+  ctx->phase_recs.clear();
+  float tot = 0.f;
+  CK(cudaEventElapsedTime(&tot, t0, t1));
+  for (int i = 0; i < 5; ++i) out->phase_s[i] = ms[i] * 1e-3;
+  out->total_s = tot * 1e-3;
+}
+
+// Turns per-call phase timing on for a scope (and drops the records of a
+// call that failed part-way).
+struct PhaseTimingScope {
+  fmv_ctx* ctx;
+  PhaseTimingScope(fmv_ctx* c, bool on) : ctx(c) {
+    for (auto& r : ctx->phase_recs) {
+      ctx->ev_pool.push_back(r.a);
+      ctx->ev_pool.push_back(r.b);
+    }
+    ctx->phase_recs.clear();
+    ctx->phase_timing = on;
+  }
+  ~PhaseTimingScope() { ctx->phase_timing = false; }
+};
 
 // Launch with programmatic dependent launch allowed (FMV_PDL=0 disables).
 template <class... KArgs, class... Args>
@@ -458,11 +580,7 @@ void r2c_reg_launch(fmv_ctx* ctx, const Tin* in, long in_ss, long nseries, int n
   const long grid = (nseries + S - 1) / S;
   constexpr size_t smem = r2c_reg_smem<C, RX, NP, S>();
   prep_smem((const void*)k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>, smem);
-  static std::once_flag once;  // ask for the max carveout so more CTAs fit per SM
-  std::call_once(once, [] {
-    CK(cudaFuncSetAttribute((const void*)k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>,
-                            cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  });
+  prep_carveout((const void*)k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>);
   launch(ctx, 0, [&] {
     launch_pdl(k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>, dim3((unsigned)grid), dim3(S * RegPlan<RX, NP>::NR), smem,
                ctx->stream, in, in_ss, nseries, nvalid, vec, static_cast<typename PT<C2>::cplx*>(out), out_ks, tw);
@@ -533,11 +651,7 @@ void c2r_reg_launch(fmv_ctx* ctx, const void* in, long in_ks, long nseries, int 
   using Cr = typename CT<typename PT<C3>::real>::c;
   constexpr size_t smem = c2r_reg_smem<Cr, RX, NP, S>();
   prep_smem((const void*)k_c2r_reg<C3, C4, Tout, RX, NP, S>, smem);
-  static std::once_flag once;
-  std::call_once(once, [] {
-    CK(cudaFuncSetAttribute((const void*)k_c2r_reg<C3, C4, Tout, RX, NP, S>,
-                            cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  });
+  prep_carveout((const void*)k_c2r_reg<C3, C4, Tout, RX, NP, S>);
   launch(ctx, 3, [&] {
     launch_pdl(k_c2r_reg<C3, C4, Tout, RX, NP, S>, dim3((unsigned)grid), dim3(S * RegPlan<RX, NP>::NR), smem,
                ctx->stream, static_cast<const C*>(in), in_ks, nseries, nout, vec, out, out_ss, tw);
@@ -835,8 +949,9 @@ struct StreamSwap {
 };
 
 struct HostIO {
-  const double* h_in = nullptr;  // copy in (overlapped) to the device `in` buffer
-  double* h_out = nullptr;       // copy out (overlapped) from the device `out` buffer
+  const void* h_in = nullptr;  // copy in (overlapped) to the device `in` buffer
+  double* h_out = nullptr;     // copy out (overlapped) from the device `out` buffer
+  size_t in_elem = 8;          // bytes per input element (a cfg[0] payload may be float / half)
 };
 
 cudaStream_t copy_stream(fmv_ctx* ctx) {
@@ -854,8 +969,7 @@ cudaEvent_t chunk_event(fmv_ctx* ctx, int i) {
 // host input is copied into `in` chunk by chunk (F) and the output leaves
 // chunk by chunk (F*) on a copy stream, overlapped with the SBGEMV.
 void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5>& p, const void* in,
-              int payload_prec, double* out, cudaEvent_t ev_r2c = nullptr, cudaEvent_t ev_gemv = nullptr,
-              const HostIO* hio = nullptr) {
+              int payload_prec, double* out, const HostIO* hio = nullptr) {
   fmv_op* op = const_cast<fmv_op*>(cop);
   const bool fwd = kind == FMV_FORWARD;
   const long nt = (long)op->nt, nb = (long)op->nb();
@@ -933,57 +1047,66 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
       // 200-thread r2c CTA fits next to the one-CTA-per-SM SBGEMV) instead
       // of serializing with it on the matvec stream.
       const bool ovl = env_int("FMV_E2E_OVERLAP", 1) != 0;
-      for (int c = 0; c < C; ++c) {
+      auto issue_in = [&](int c) {
         const long j0 = chunk_edge(n, c, C), j1 = chunk_edge(n, c + 1, C);
-        CK(cudaMemcpyAsync(const_cast<double*>(static_cast<const double*>(in)) + j0 * nt, hio->h_in + j0 * nt,
-                           (size_t)(j1 - j0) * nt * sizeof(double), cudaMemcpyHostToDevice, ks));
+        const size_t ie = hio->in_elem;
+        copy_async(ctx, 0, const_cast<unsigned char*>(static_cast<const unsigned char*>(in)) + j0 * nt * ie,
+                   static_cast<const unsigned char*>(hio->h_in) + j0 * nt * ie, (size_t)(j1 - j0) * nt * ie,
+                   cudaMemcpyHostToDevice, ks);
         if (ovl) {
           StreamSwap sw(ctx, ks);
           r2c_series(j0, j1);
         }
         CK(cudaEventRecord(chunk_event(ctx, c), ks));
-      }
+      };
+      // Chunk c+1's copy is issued after chunk c's SBGEMV is enqueued: from a
+      // pageable buffer cudaMemcpyAsync blocks the host until the data is
+      // staged, and this order keeps the SBGEMV running meanwhile.
+      issue_in(0);
       for (int c = 0; c < C; ++c) {
         CK(cudaStreamWaitEvent(cs, chunk_event(ctx, c), 0));
         if (!ovl) r2c_series(chunk_edge(n, c, C), chunk_edge(n, c + 1, C));
         gemv_chunk(c);
+        if (c + 1 < C) issue_in(c + 1);
       }
-      if (ev_r2c) CK(cudaEventRecord(ev_r2c, cs));
     } else {
       r2c_series(0, n_in);
-      if (ev_r2c) CK(cudaEventRecord(ev_r2c, cs));
       for (int c = 0; c < C; ++c) gemv_chunk(c);
     }
-    if (ev_gemv) CK(cudaEventRecord(ev_gemv, cs));
     c2r_series(0, n_out);
-    if (h_out) CK(cudaMemcpyAsync(hio->h_out, out, (size_t)n_out * nt * sizeof(double), cudaMemcpyDeviceToHost, cs));
+    if (h_out) copy_async(ctx, 4, hio->h_out, out, (size_t)n_out * nt * sizeof(double), cudaMemcpyDeviceToHost, cs);
   } else {
     if (h_in)
-      CK(cudaMemcpyAsync(const_cast<double*>(static_cast<const double*>(in)), hio->h_in,
-                         (size_t)n_in * nt * sizeof(double), cudaMemcpyHostToDevice, cs));
+      copy_async(ctx, 0, const_cast<void*>(in), hio->h_in, (size_t)n_in * nt * hio->in_elem, cudaMemcpyHostToDevice,
+                 cs);
     r2c_series(0, n_in);
-    if (ev_r2c) CK(cudaEventRecord(ev_r2c, cs));
     if (h_out) {
       cudaStream_t ks = copy_stream(ctx);
       // (chunk c's c2r stays on the matvec stream: on the copy stream, running
       // alongside the SBGEMV of chunk c+1, it slowed F* from 1.37 to 1.62 ms
       // with a full grid and to 2.13 ms with one-CTA-per-SM sub-launches --
       // the c2r's shared-memory traffic competes with the ConjTrans consumers)
+      // Chunk c's copy-out is issued after chunk c+1's SBGEMV is enqueued (a
+      // pageable destination makes cudaMemcpyAsync block the host until the
+      // copy is done).
+      auto issue_out = [&](int c) {
+        const long j0 = chunk_edge(n, c, C), j1 = chunk_edge(n, c + 1, C);
+        CK(cudaStreamWaitEvent(ks, chunk_event(ctx, c), 0));
+        copy_async(ctx, 4, hio->h_out + j0 * nt, out + j0 * nt, (size_t)(j1 - j0) * nt * sizeof(double),
+                   cudaMemcpyDeviceToHost, ks);
+      };
       for (int c = 0; c < C; ++c) {
         const long j0 = chunk_edge(n, c, C), j1 = chunk_edge(n, c + 1, C);
         gemv_chunk(c);
         c2r_series(j0, j1);
         CK(cudaEventRecord(chunk_event(ctx, c), cs));
-        CK(cudaStreamWaitEvent(ks, chunk_event(ctx, c), 0));
-        CK(cudaMemcpyAsync(hio->h_out + j0 * nt, out + j0 * nt, (size_t)(j1 - j0) * nt * sizeof(double),
-                           cudaMemcpyDeviceToHost, ks));
+        if (c > 0) issue_out(c - 1);
       }
+      issue_out(C - 1);
       CK(cudaEventRecord(chunk_event(ctx, 33), ks));
       CK(cudaStreamWaitEvent(cs, chunk_event(ctx, 33), 0));
-      if (ev_gemv) CK(cudaEventRecord(ev_gemv, cs));
     } else {
       for (int c = 0; c < C; ++c) gemv_chunk(c);
-      if (ev_gemv) CK(cudaEventRecord(ev_gemv, cs));
       c2r_series(0, n_out);
     }
   }
@@ -1164,8 +1287,8 @@ unsigned grid_for(long n, int block, int dev) {
 
 void materialize(fmv_ctx* ctx, fmv_op* op, int prec) {
   std::lock_guard<std::mutex> lk(op->mu);
-  if (prec == PS && op->bins_s) return;
-  if (prec == PH && op->bins_h) return;
+  std::atomic<void*>& slot = prec == PS ? op->bins_s : op->bins_h;
+  if (slot.load(std::memory_order_acquire)) return;
   const long ncols = (long)(op->nb() * op->nm);
   const long nd = (long)op->nd;
   // pad the leading dimension so every column starts 16-byte aligned (TMA)
@@ -1173,22 +1296,26 @@ void materialize(fmv_ctx* ctx, fmv_op* op, int prec) {
   const size_t bytes = (size_t)ncols * lda * (prec == PS ? 8 : 4) + 256;
   void* p = nullptr;
   CK(cudaMalloc(&p, bytes));
-  if (prec == PS) {
-    launch(ctx, 4, [&] {
-      k_cast_bins<float2><<<grid_for(ncols * lda, 256, ctx->device), 256, 0, ctx->stream>>>(
-          static_cast<const double2*>(op->bins_d), static_cast<float2*>(p), ncols, nd, lda);
-    });
-    op->bins_s = p;
-    op->lda_s = (size_t)lda;
-  } else {
-    launch(ctx, 4, [&] {
-      k_cast_bins<__half2><<<grid_for(ncols * lda, 256, ctx->device), 256, 0, ctx->stream>>>(
-          static_cast<const double2*>(op->bins_d), static_cast<__half2*>(p), ncols, nd, lda);
-    });
-    op->bins_h = p;
-    op->lda_h = (size_t)lda;
+  try {
+    if (prec == PS) {
+      launch(ctx, 4, [&] {
+        k_cast_bins<float2><<<grid_for(ncols * lda, 256, ctx->device), 256, 0, ctx->stream>>>(
+            static_cast<const double2*>(op->bins_d), static_cast<float2*>(p), ncols, nd, lda);
+      });
+    } else {
+      launch(ctx, 4, [&] {
+        k_cast_bins<__half2><<<grid_for(ncols * lda, 256, ctx->device), 256, 0, ctx->stream>>>(
+            static_cast<const double2*>(op->bins_d), static_cast<__half2*>(p), ncols, nd, lda);
+      });
+    }
+    // the copy is complete before any other context can see it
+    CK(cudaStreamSynchronize(ctx->stream));
+  } catch (...) {
+    cudaFree(p);
+    throw;
   }
-  CK(cudaStreamSynchronize(ctx->stream));
+  (prec == PS ? op->lda_s : op->lda_h) = (size_t)lda;
+  slot.store(p, std::memory_order_release);
   g_casts.fetch_add(1, std::memory_order_relaxed);  // ensure_single's cast_buffer (operator.hpp:72)
 }
 
@@ -1197,14 +1324,22 @@ const void* op_bins(fmv_ctx* ctx, fmv_op* op, int prec, long* lda) {
     *lda = (long)op->nd;
     return op->bins_d;
   }
-  if (prec == PS) {
-    if (!op->bins_s) materialize(ctx, op, PS);
-    *lda = (long)op->lda_s;
-    return op->bins_s;
+  std::atomic<void*>& slot = prec == PS ? op->bins_s : op->bins_h;
+  void* p = slot.load(std::memory_order_acquire);
+  if (!p) {
+    materialize(ctx, op, prec);
+    p = slot.load(std::memory_order_acquire);
   }
-  if (!op->bins_h) materialize(ctx, op, PH);
-  *lda = (long)op->lda_h;
-  return op->bins_h;
+  *lda = (long)(prec == PS ? op->lda_s : op->lda_h);
+  return p;
+}
+
+// Every entry point that pairs a context with an operator: the operator's
+// memory lives on one device and is only valid there.
+void check_same_device(const fmv_ctx* ctx, const fmv_op* op) {
+  if (op->device != ctx->device)
+    fail(FMV_EINVAL, "operator lives on device " + std::to_string(op->device) + " but the context is on device " +
+                         std::to_string(ctx->device));
 }
 
 }  // namespace
@@ -1213,46 +1348,173 @@ const void* op_bins(fmv_ctx* ctx, fmv_op* op, int prec, long* lda) {
 // C ABI
 // ======================================================================
 namespace {
+// ---- collectives of the partitioned matvecs (partition.hpp:157-217) ----
+
 // Round `in` (n doubles, valid on the group root) to cfg[0] precision once and
-// broadcast it over `comm` (group size gsize): the payload semantics of
-// partition.hpp:196-206. Returns the payload pointer and its precision.
-std::pair<const void*, int> bcast_payload(fmv_ctx* ctx, void* comm, int gsize, bool root, const double* in, long n,
-                                          int p0) {
+// broadcast it over `comm`: the payload semantics of partition.hpp:196-206.
+// Returns the payload pointer and its precision. Charged to phase [0]
+// (partition.hpp:204-206).
+std::pair<const void*, int> bcast_payload(fmv_ctx* ctx, void* comm, bool root, const double* in, long n, int p0) {
   cudaStream_t s = ctx->stream;
   if (p0 == PD) {
     if (!comm) return {in, PD};
     ctx->payload.ensure(n * sizeof(double));
-    if (root) CK(cudaMemcpyAsync(ctx->payload.p, in, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    nck(nccl().broadcast(ctx->payload.p, ctx->payload.p, n, kNcclDouble, 0, comm, s), "ncclBroadcast");
+    phase_span(ctx, s, 0, [&] {
+      if (root) CK(cudaMemcpyAsync(ctx->payload.p, in, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      nck(nccl().broadcast(ctx->payload.p, ctx->payload.p, n, kNcclDouble, 0, comm, s), "ncclBroadcast");
+    });
     return {ctx->payload.p, PD};
   }
   ctx->payload.ensure(n * sizeof(float));
   if (root) {
     if (p0 == PS)
-      launch(ctx, 4, [&] { k_d2f<<<grid_for(n, 256, ctx->device), 256, 0, s>>>(in, static_cast<float*>(ctx->payload.p), n); });
+      launch(ctx, 4, [&] { k_d2f<<<grid_for(n, 256, ctx->device), 256, 0, s>>>(in, static_cast<float*>(ctx->payload.p), n); }, 0);
     else
-      launch(ctx, 4, [&] { k_d2h<<<grid_for(n, 256, ctx->device), 256, 0, s>>>(in, static_cast<__half*>(ctx->payload.p), n); });
+      launch(ctx, 4, [&] { k_d2h<<<grid_for(n, 256, ctx->device), 256, 0, s>>>(in, static_cast<__half*>(ctx->payload.p), n); }, 0);
     g_casts.fetch_add(1, std::memory_order_relaxed);  // partition.hpp:203
   }
   if (comm)
-    nck(nccl().broadcast(ctx->payload.p, ctx->payload.p, n, p0 == PS ? kNcclFloat : kNcclHalf, 0, comm, s),
-        "ncclBroadcast");
+    phase_span(ctx, s, 0, [&] {
+      nck(nccl().broadcast(ctx->payload.p, ctx->payload.p, n, p0 == PS ? kNcclFloat : kNcclHalf, 0, comm, s),
+          "ncclBroadcast");
+    });
   return {ctx->payload.p, p0};
 }
 
-// Sum the n-double partial `buf` over `comm` in cfg[4] precision (partition.hpp:175-177).
-void allreduce_prec(fmv_ctx* ctx, void* comm, int gsize, double* buf, long n, int p4) {
-  if (!comm) return;
-  cudaStream_t s = ctx->stream;
-  if (p4 == PD) {
-    nck(nccl().all_reduce(buf, buf, n, kNcclDouble, kNcclSum, comm, s), "ncclAllReduce");
+// Fixed left-balanced pairwise tree over the p gathered partials, in T
+// (partition.hpp:84-107 / tree_reduce): round w pairs (k, k+w) for k a
+// multiple of 2w -- p=4 gives ((b0+b1)+(b2+b3)), p=3 ((b0+b1)+b2) -- and the
+// root is widened to double. One thread per element; G is p x n, rank-major.
+template <class T>
+__global__ void k_tree_reduce(T* __restrict__ G, long n, int p, double* __restrict__ out) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    for (int w = 1; w < p; w *= 2)
+      for (int k = 0; k + w < p; k += 2 * w) G[(long)k * n + i] = G[(long)k * n + i] + G[(long)(k + w) * n + i];
+    out[i] = (double)G[i];
+  }
+}
+
+// Sum the n-double partial `buf` over `comm` (gsize ranks) in cfg[4]
+// precision (partition.hpp:175-177): the partials are all-gathered in rank
+// order and reduced on the device with the reference's fixed tree, so every
+// rank gets the bits of the in-process tree_reduce (NCCL's own all-reduce
+// order depends on the algorithm it picks). The message is nd*nt values
+// (0.8 MB at C2), so gathering p of them costs little. Charged to phase [4]
+// (partition.hpp:178-180). gsize == 1: nothing to do.
+void reduce_partials(fmv_ctx* ctx, void* comm, int gsize, int grank, double* buf, long n, int p4) {
+  if (!comm || gsize < 2) {
+    // one worker: tree_reduce<float> still casts the lone partial to float and
+    // back (2 casts); its value is already float-representable (the unpad
+    // rounded it to cfg[4]), so only the counter moves
+    if (p4 != PD) g_casts.fetch_add(2, std::memory_order_relaxed);
     return;
   }
-  ctx->red.ensure(n * sizeof(float));
-  float* f = static_cast<float*>(ctx->red.p);
-  launch(ctx, 4, [&] { k_d2f<<<grid_for(n, 256, ctx->device), 256, 0, s>>>(buf, f, n); });
-  nck(nccl().all_reduce(f, f, n, kNcclFloat, kNcclSum, comm, s), "ncclAllReduce");
-  launch(ctx, 4, [&] { k_f2d<<<grid_for(n, 256, ctx->device), 256, 0, s>>>(f, buf, n); });
+  cudaStream_t s = ctx->stream;
+  if (p4 == PD) {
+    ctx->red.ensure((size_t)gsize * n * sizeof(double));
+    double* G = static_cast<double*>(ctx->red.p);
+    phase_span(ctx, s, 4, [&] { nck(nccl().all_gather(buf, G, n, kNcclDouble, comm, s), "ncclAllGather"); });
+    launch(ctx, 4, [&] { k_tree_reduce<double><<<grid_for(n, 256, ctx->device), 256, 0, s>>>(G, n, gsize, buf); }, 4);
+    return;
+  }
+  // cfg[4] single: every partial is cast to float (one cast per rank), the
+  // tree runs in float and the root is cast back to double (counted once,
+  // on group rank 0), as tree_reduce_impl<float> counts them in one process.
+  ctx->red.ensure((size_t)(gsize + 1) * n * sizeof(float));
+  float* G = static_cast<float*>(ctx->red.p);
+  float* mine = G + (size_t)gsize * n;
+  launch(ctx, 4, [&] { k_d2f<<<grid_for(n, 256, ctx->device), 256, 0, s>>>(buf, mine, n); }, 4);
+  phase_span(ctx, s, 4, [&] { nck(nccl().all_gather(mine, G, n, kNcclFloat, comm, s), "ncclAllGather"); });
+  launch(ctx, 4, [&] { k_tree_reduce<float><<<grid_for(n, 256, ctx->device), 256, 0, s>>>(G, n, gsize, buf); }, 4);
+  g_casts.fetch_add(grank == 0 ? 2 : 1, std::memory_order_relaxed);
+}
+
+double env_seconds(const char* name, double dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atof(v) : dflt;
+}
+
+// Wait for the matvec stream while watching the communicators: an
+// asynchronous NCCL error (a peer died, a network failure) or no progress
+// within FMV_NCCL_TIMEOUT_S seconds (default 600) aborts the communicators
+// -- which also unblocks kernels stuck waiting for a dead peer -- and fails
+// the call with FMV_ENCCL instead of hanging forever. The context then has
+// no communicator; fmv_comm_init must be called again.
+void comm_sync(fmv_ctx* ctx) {
+  void* comms[3] = {ctx->comm, ctx->row_comm, ctx->col_comm};
+  const bool any = comms[0] || comms[1] || comms[2];
+  if (!any) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    return;
+  }
+  const double limit = env_seconds("FMV_NCCL_TIMEOUT_S", 600.0);
+  const auto t0 = std::chrono::steady_clock::now();
+  auto abort_all = [&](const std::string& why) {
+    for (void** c : {&ctx->row_comm, &ctx->col_comm, &ctx->comm}) {
+      if (*c) {
+        if (nccl().comm_abort) nccl().comm_abort(*c);
+        else if (nccl().comm_destroy) nccl().comm_destroy(*c);
+      }
+      *c = nullptr;
+    }
+    ctx->nranks = 1;
+    ctx->rank = 0;
+    (void)cudaStreamSynchronize(ctx->stream);  // drains once the aborted kernels return
+    (void)cudaGetLastError();
+    fail(FMV_ENCCL, why);
+  };
+  for (long it = 0;; ++it) {
+    const cudaError_t q = cudaStreamQuery(ctx->stream);
+    if (q == cudaSuccess) return;
+    if (q != cudaErrorNotReady) CK(q);
+    if (nccl().get_async_error) {
+      for (void* c : comms) {
+        if (!c) continue;
+        int e = 0;
+        const int rc = nccl().get_async_error(c, &e);
+        if (rc == 0 && e != 0 && e != 7 /* ncclInProgress */)
+          abort_all(std::string("NCCL asynchronous error: ") + (nccl().err ? nccl().err(e) : "nccl error"));
+      }
+    }
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > limit)
+      abort_all("NCCL collective did not complete within " + std::to_string(limit) +
+                " s (FMV_NCCL_TIMEOUT_S); communicator aborted");
+    if (it < 2000) std::this_thread::yield();
+    else std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+}  // namespace
+
+namespace {
+// The blocking matvec behind fmv_matvec / fmv_matvec_payload. Host I/O
+// always takes the overlapped path: the input copy and the output copy run
+// chunk by chunk on a copy stream beside the SBGEMV. With
+// `times`, each kernel / copy is bracketed by CUDA events and the
+// PhaseTimings are the per-phase busy times (phases overlap on the host-I/O
+// path, so their sum may exceed total_s, the wall time of the call).
+void matvec_blocking(fmv_ctx* ctx, const fmv_op* op, int kind, const std::array<int, 5>& p, int payload_prec,
+                     const void* in, double* out, bool io_on_device, fmv_phase_times* times) {
+  const bool fwd = kind == FMV_FORWARD;
+  const size_t in_elem = payload_prec < 0 || payload_prec == PD ? 8 : payload_prec == PS ? 4 : 2;
+  const size_t n_in = (fwd ? op->nm : op->nd) * op->nt, n_out = (fwd ? op->nd : op->nm) * op->nt;
+  cudaStream_t s = ctx->stream;
+  PhaseTimingScope pts(ctx, times != nullptr);
+  if (times) CK(cudaEventRecord(ctx->te[0], s));
+  if (io_on_device) {
+    pipeline(ctx, op, kind, p, in, payload_prec, out);
+  } else {
+    ctx->io_in.ensure(n_in * in_elem);
+    ctx->io_out.ensure(n_out * sizeof(double));
+    HostIO hio;
+    hio.h_in = in;
+    hio.h_out = out;
+    hio.in_elem = in_elem;
+    pipeline(ctx, op, kind, p, ctx->io_in.p, payload_prec, static_cast<double*>(ctx->io_out.p), &hio);
+  }
+  if (times) CK(cudaEventRecord(ctx->te[1], s));
+  CK(cudaStreamSynchronize(s));
+  if (times) collect_phase_times(ctx, ctx->te[0], ctx->te[1], times);
 }
 }  // namespace
 
@@ -1302,7 +1564,8 @@ int fmv_ctx_destroy(fmv_ctx* ctx) {
     }
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     for (auto e : ctx->te) cudaEventDestroy(e);
-    if (ctx->comm && nccl().comm_destroy) nccl().comm_destroy(ctx->comm);
+    for (void* c : {ctx->row_comm, ctx->col_comm, ctx->comm})
+      if (c && nccl().comm_destroy) nccl().comm_destroy(c);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -1385,8 +1648,8 @@ int fmv_op_destroy(fmv_op* op) {
     if (!op) return;
     DeviceGuard dg(op->device);
     if (op->bins_d) cudaFree(op->bins_d);
-    if (op->bins_s) cudaFree(op->bins_s);
-    if (op->bins_h) cudaFree(op->bins_h);
+    if (void* p = op->bins_s.load()) cudaFree(p);
+    if (void* p = op->bins_h.load()) cudaFree(p);
     delete op;
   });
 }
@@ -1403,6 +1666,7 @@ int fmv_op_dims(const fmv_op* op, size_t* nm, size_t* nd, size_t* nt) {
 int fmv_op_materialize(fmv_ctx* ctx, fmv_op* op, char prec) {
   return guarded([&] {
     if (!ctx || !op) fail(FMV_EINVAL, "null argument");
+    check_same_device(ctx, op);
     if (prec != 's' && prec != 'h') fail(FMV_EINVAL, "fmv_op_materialize: prec must be 's' or 'h'");
     DeviceGuard dg(ctx->device);
     materialize(ctx, op, prec_of(prec));
@@ -1412,8 +1676,8 @@ int fmv_op_materialize(fmv_ctx* ctx, fmv_op* op, char prec) {
 int fmv_op_has(const fmv_op* op, char prec) {
   if (!op) return 0;
   if (prec == 'd') return op->bins_d != nullptr;
-  if (prec == 's') return op->bins_s != nullptr;
-  if (prec == 'h') return op->bins_h != nullptr;
+  if (prec == 's') return op->bins_s.load(std::memory_order_acquire) != nullptr;
+  if (prec == 'h') return op->bins_h.load(std::memory_order_acquire) != nullptr;
   return 0;
 }
 
@@ -1421,13 +1685,15 @@ int fmv_op_download_bins(fmv_ctx* ctx, const fmv_op* cop, char prec, void* host_
   return guarded([&] {
     if (!ctx || !cop || !host_out) fail(FMV_EINVAL, "null argument");
     fmv_op* op = const_cast<fmv_op*>(cop);
+    check_same_device(ctx, op);
     DeviceGuard dg(ctx->device);
     const size_t ncols = op->nb() * op->nm;
     if (prec == 'd') {
       CK(cudaMemcpy(host_out, op->bins_d, ncols * op->nd * sizeof(double2), cudaMemcpyDeviceToHost));
     } else if (prec == 's') {
-      if (!op->bins_s) materialize(ctx, op, PS);
-      CK(cudaMemcpy2D(host_out, op->nd * sizeof(float2), op->bins_s, op->lda_s * sizeof(float2),
+      long lda = 0;
+      const void* bs = op_bins(ctx, op, PS, &lda);
+      CK(cudaMemcpy2D(host_out, op->nd * sizeof(float2), bs, (size_t)lda * sizeof(float2),
                       op->nd * sizeof(float2), ncols, cudaMemcpyDeviceToHost));
     } else {
       fail(FMV_EINVAL, "fmv_op_download_bins: prec must be 'd' or 's'");
@@ -1439,8 +1705,8 @@ size_t fmv_op_device_bytes(const fmv_op* op) {
   if (!op) return 0;
   const size_t ncols = op->nb() * op->nm;
   size_t b = ncols * op->nd * sizeof(double2);
-  if (op->bins_s) b += ncols * op->lda_s * sizeof(float2);
-  if (op->bins_h) b += ncols * op->lda_h * sizeof(__half2);
+  if (op->bins_s.load()) b += ncols * op->lda_s * sizeof(float2);
+  if (op->bins_h.load()) b += ncols * op->lda_h * sizeof(__half2);
   return b;
 }
 
@@ -1448,6 +1714,7 @@ int fmv_matvec_block_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char*
                            double* d_out) {
   return guarded([&] {
     if (!ctx || !op || !d_in || !d_out) fail(FMV_EINVAL, "fmv_matvec_block_async: null argument");
+    check_same_device(ctx, op);
     if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
     if (nrhs == 0) return;
     const auto p = parse_cfg(cfg);
@@ -1459,6 +1726,7 @@ int fmv_matvec_block(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, 
                      double* out, int io_on_device) {
   return guarded([&] {
     if (!ctx || !op || !in || !out) fail(FMV_EINVAL, "fmv_matvec_block: null argument");
+    check_same_device(ctx, op);
     if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
     if (nrhs == 0) return;
     const auto p = parse_cfg(cfg);
@@ -1483,6 +1751,7 @@ int fmv_matvec_block(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, 
 int fmv_matvec_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* d_in, double* d_out) {
   return guarded([&] {
     if (!ctx || !op || !d_in || !d_out) fail(FMV_EINVAL, "fmv_matvec_async: null argument");
+    check_same_device(ctx, op);
     if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
     const auto p = parse_cfg(cfg);
     DeviceGuard dg(ctx->device);
@@ -1495,50 +1764,23 @@ int fmv_matvec(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const 
   return guarded([&] {
     if (!ctx || !op || !in || !out) fail(FMV_EINVAL, "fmv_matvec: null argument");
     if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
+    check_same_device(ctx, op);
     const auto p = parse_cfg(cfg);
     DeviceGuard dg(ctx->device);
-    const bool fwd = kind == FMV_FORWARD;
-    const size_t n_in = (fwd ? op->nm : op->nd) * op->nt, n_out = (fwd ? op->nd : op->nm) * op->nt;
-    const double* din = in;
-    double* dout = out;
-    cudaStream_t s = ctx->stream;
-    auto* te = ctx->te;
-    if (!io_on_device) {
-      ctx->io_in.ensure(n_in * sizeof(double));
-      ctx->io_out.ensure(n_out * sizeof(double));
-      din = static_cast<const double*>(ctx->io_in.p);
-      dout = static_cast<double*>(ctx->io_out.p);
-    }
-    if (!io_on_device && !times) {
-      // host I/O: copies overlapped with the SBGEMV of neighbouring column chunks
-      const HostIO hio{in, out};
-      pipeline(ctx, op, kind, p, din, -1, dout, nullptr, nullptr, &hio);
-      CK(cudaStreamSynchronize(s));
-      return;
-    }
-    // timed (PhaseTimings) path: copies serialised so each phase has its own span
-    if (times) CK(cudaEventRecord(te[0], s));
-    if (!io_on_device) CK(cudaMemcpyAsync(ctx->io_in.p, in, n_in * sizeof(double), cudaMemcpyHostToDevice, s));
-    if (times) CK(cudaEventRecord(te[1], s));
-    pipeline(ctx, op, kind, p, din, -1, dout, times ? te[2] : nullptr, times ? te[3] : nullptr);
-    if (times) CK(cudaEventRecord(te[4], s));
-    if (!io_on_device) CK(cudaMemcpyAsync(out, dout, n_out * sizeof(double), cudaMemcpyDeviceToHost, s));
-    if (times) CK(cudaEventRecord(te[5], s));
-    CK(cudaStreamSynchronize(s));
-    if (times) {
-      float ms[5];
-      CK(cudaEventElapsedTime(&ms[0], te[0], te[1]));
-      CK(cudaEventElapsedTime(&ms[1], te[1], te[2]));
-      CK(cudaEventElapsedTime(&ms[2], te[2], te[3]));
-      CK(cudaEventElapsedTime(&ms[3], te[3], te[4]));
-      CK(cudaEventElapsedTime(&ms[4], te[4], te[5]));
-      double tot = 0;
-      for (int i = 0; i < 5; ++i) {
-        times->phase_s[i] = ms[i] * 1e-3;
-        tot += times->phase_s[i];
-      }
-      times->total_s = tot;
-    }
+    matvec_blocking(ctx, op, kind, p, -1, in, out, io_on_device != 0, times);
+  });
+}
+
+int fmv_matvec_payload(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, char payload_prec, const void* in,
+                       double* out, int io_on_device, fmv_phase_times* times) {
+  return guarded([&] {
+    if (!ctx || !op || !in || !out) fail(FMV_EINVAL, "fmv_matvec_payload: null argument");
+    if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
+    check_same_device(ctx, op);
+    const auto p = parse_cfg(cfg);
+    const int pp = prec_of(payload_prec);
+    DeviceGuard dg(ctx->device);
+    matvec_blocking(ctx, op, kind, p, pp, in, out, io_on_device != 0, times);
   });
 }
 
@@ -1635,6 +1877,14 @@ int fmv_comm_init(fmv_ctx* ctx, int nranks, int rank, const void* id128) {
   });
 }
 
+int fmv_comm_size(const fmv_ctx* ctx, int* nranks, int* rank) {
+  return guarded([&] {
+    if (!ctx) fail(FMV_EINVAL, "null ctx");
+    if (nranks) *nranks = ctx->comm ? ctx->nranks : 1;
+    if (rank) *rank = ctx->comm ? ctx->rank : 0;
+  });
+}
+
 int fmv_comm_destroy(fmv_ctx* ctx) {
   return guarded([&] {
     if (!ctx) fail(FMV_EINVAL, "null ctx");
@@ -1671,109 +1921,45 @@ int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* op, int kind, const char*
   return guarded([&] {
     if (!ctx || !op || !out) fail(FMV_EINVAL, "fmv_matvec_partitioned: null argument");
     if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
+    check_same_device(ctx, op);
     const auto p = parse_cfg(cfg);
     DeviceGuard dg(ctx->device);
     cudaStream_t s = ctx->stream;
     const bool fwd = kind == FMV_FORWARD;
     const size_t nt = op->nt;
     const size_t n_in = (fwd ? op->nm : op->nd) * nt, n_out = (fwd ? op->nd : op->nm) * nt;
-    auto* te = ctx->te;
-    if (times) CK(cudaEventRecord(te[0], s));
-    const double* din = in;
-    double* dout = out;
     const bool have_in = fwd || ctx->rank == 0;
     if (have_in && !in) fail(FMV_EINVAL, "fmv_matvec_partitioned: null input");
-    // Host I/O without PhaseTimings: the shard pipeline overlaps the big copy
-    // with its SBGEMV column chunks (F: the m slice in; F*: the m slice out),
-    // as fmv_matvec does.
-    const bool chunked = !io_on_device && !times;
+    PhaseTimingScope pts(ctx, times != nullptr);
+    if (times) CK(cudaEventRecord(ctx->te[0], s));
+    const double* din = in;
+    double* dout = out;
+    // Host I/O: the shard pipeline overlaps the big copy with its SBGEMV
+    // column chunks (F: the m slice in; F*: the m slice out), as fmv_matvec.
     HostIO hio{};
     if (!io_on_device) {
       ctx->io_in.ensure(std::max(n_in, op->nd * nt) * sizeof(double));
       ctx->io_out.ensure(n_out * sizeof(double));
-      if (chunked && fwd) hio.h_in = in;
-      else if (have_in) CK(cudaMemcpyAsync(ctx->io_in.p, in, n_in * sizeof(double), cudaMemcpyHostToDevice, s));
-      if (chunked && !fwd) hio.h_out = out;
+      if (fwd) hio.h_in = in;
+      else if (have_in) copy_async(ctx, 0, ctx->io_in.p, in, n_in * sizeof(double), cudaMemcpyHostToDevice, s);
+      if (!fwd) hio.h_out = out;
       din = static_cast<const double*>(ctx->io_in.p);
       dout = static_cast<double*>(ctx->io_out.p);
     }
-    if (times) CK(cudaEventRecord(te[1], s));
+    const HostIO* hp = io_on_device ? nullptr : &hio;
     if (fwd) {
       // partition.hpp:157-182: full-length partial d per rank, summed in cfg[4].
-      pipeline(ctx, op, kind, p, din, -1, dout, nullptr, nullptr, chunked ? &hio : nullptr);
-      if (times) CK(cudaEventRecord(te[2], s));
-      if (ctx->comm) {
-        const long nd = (long)(op->nd * nt);
-        if (p[4] == PD) {
-          nck(nccl().all_reduce(dout, dout, nd, kNcclDouble, kNcclSum, ctx->comm, s), "ncclAllReduce");
-        } else {
-          ctx->payload.ensure(nd * sizeof(float));
-          float* f = static_cast<float*>(ctx->payload.p);
-          launch(ctx, 4, [&] { k_d2f<<<grid_for(nd, 256, ctx->device), 256, 0, s>>>(dout, f, nd); });
-          nck(nccl().all_reduce(f, f, nd, kNcclFloat, kNcclSum, ctx->comm, s), "ncclAllReduce");
-          launch(ctx, 4, [&] { k_f2d<<<grid_for(nd, 256, ctx->device), 256, 0, s>>>(f, dout, nd); });
-        }
-      }
-      if (times) CK(cudaEventRecord(te[3], s));
+      pipeline(ctx, op, kind, p, din, -1, dout, hp);
+      reduce_partials(ctx, ctx->comm, ctx->nranks, ctx->rank, dout, (long)(op->nd * nt), p[4]);
+      if (!io_on_device) copy_async(ctx, 4, out, dout, n_out * sizeof(double), cudaMemcpyDeviceToHost, s);
     } else {
       // partition.hpp:187-217: cast d to cfg[0] once, broadcast, pad from payload.
-      const long nd = (long)(op->nd * nt);
-      const void* pay = din;
-      int pprec = PD;
-      if (p[0] == PD) {
-        if (ctx->comm) {
-          ctx->payload.ensure(nd * sizeof(double));
-          if (ctx->rank == 0)
-            CK(cudaMemcpyAsync(ctx->payload.p, din, nd * sizeof(double), cudaMemcpyDeviceToDevice, s));
-          nck(nccl().broadcast(ctx->payload.p, ctx->payload.p, nd, kNcclDouble, 0, ctx->comm, s), "ncclBroadcast");
-          pay = ctx->payload.p;
-        }
-      } else {
-        ctx->payload.ensure(nd * sizeof(float));
-        if (ctx->rank == 0) {
-          if (p[0] == PS)
-            launch(ctx, 4, [&] {
-              k_d2f<<<grid_for(nd, 256, ctx->device), 256, 0, s>>>(din, static_cast<float*>(ctx->payload.p), nd);
-            });
-          else
-            launch(ctx, 4, [&] {
-              k_d2h<<<grid_for(nd, 256, ctx->device), 256, 0, s>>>(din, static_cast<__half*>(ctx->payload.p), nd);
-            });
-          g_casts.fetch_add(1, std::memory_order_relaxed);  // partition.hpp:203
-        }
-        if (ctx->comm)
-          nck(nccl().broadcast(ctx->payload.p, ctx->payload.p, nd, p[0] == PS ? kNcclFloat : kNcclHalf, 0, ctx->comm,
-                               s),
-              "ncclBroadcast");
-        pay = ctx->payload.p;
-        pprec = p[0];
-      }
-      if (times) CK(cudaEventRecord(te[2], s));
-      pipeline(ctx, op, kind, p, pay, pprec, dout, nullptr, nullptr, chunked ? &hio : nullptr);
-      if (times) CK(cudaEventRecord(te[3], s));
+      const auto pay = bcast_payload(ctx, ctx->comm, ctx->rank == 0, din, (long)(op->nd * nt), p[0]);
+      pipeline(ctx, op, kind, p, pay.first, p[0] == PD && !ctx->comm ? -1 : pay.second, dout, hp);
     }
-    if (!io_on_device && !(chunked && !fwd))  // (chunked F*: the pipeline already copied the slice out)
-      CK(cudaMemcpyAsync(out, dout, n_out * sizeof(double), cudaMemcpyDeviceToHost, s));
-    if (times) CK(cudaEventRecord(te[4], s));
-    CK(cudaStreamSynchronize(s));
-    if (times) {
-      float a, b, c, d;
-      CK(cudaEventElapsedTime(&a, te[0], te[1]));
-      CK(cudaEventElapsedTime(&b, te[1], te[2]));
-      CK(cudaEventElapsedTime(&c, te[2], te[3]));
-      CK(cudaEventElapsedTime(&d, te[3], te[4]));
-      for (auto& v : times->phase_s) v = 0;
-      if (fwd) {
-        times->phase_s[0] = a * 1e-3;
-        times->phase_s[2] = b * 1e-3;  // whole fused pipeline
-        times->phase_s[4] = (c + d) * 1e-3;  // reduce + copy-out (partition.hpp:178-180)
-      } else {
-        times->phase_s[0] = (a + b) * 1e-3;  // copy-in + broadcast (partition.hpp:204-206)
-        times->phase_s[2] = c * 1e-3;
-        times->phase_s[4] = d * 1e-3;
-      }
-      times->total_s = (a + b + c + d) * 1e-3;
-    }
+    if (times) CK(cudaEventRecord(ctx->te[1], s));
+    comm_sync(ctx);
+    if (times) collect_phase_times(ctx, ctx->te[0], ctx->te[1], times);
   });
 }
 
@@ -1782,17 +1968,18 @@ int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* op, int kind, const char*
 // rank's shard is the (ri, cj) sub-block of every time block.
 // FORWARD: in = m_cj (nm_cj*nt), read on grid row 0 only; it is rounded to
 //   cfg[0] and broadcast down the column, each rank computes its partial
-//   d_ri, and the row all-reduces it in cfg[4]: out = d_ri (nd_ri*nt) on
-//   every rank of grid row ri.
+//   d_ri, and the row sums it in cfg[4] (fixed tree): out = d_ri (nd_ri*nt)
+//   on every rank of grid row ri.
 // ADJOINT: in = d_ri (nd_ri*nt), read on grid column 0 only; rounded to
-//   cfg[0] and broadcast along the row, partial m_cj all-reduced down the
-//   column in cfg[4]: out = m_cj (nm_cj*nt) on every rank of grid column cj.
+//   cfg[0] and broadcast along the row, partial m_cj summed down the column
+//   in cfg[4]: out = m_cj (nm_cj*nt) on every rank of grid column cj.
 // With pr = 1 this is the 1 x p partition (the forward input is then local).
 int fmv_matvec_partitioned_2d(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* in,
                               double* out, int io_on_device) {
   return guarded([&] {
     if (!ctx || !op || !out) fail(FMV_EINVAL, "fmv_matvec_partitioned_2d: null argument");
     if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
+    check_same_device(ctx, op);
     const auto p = parse_cfg(cfg);
     DeviceGuard dg(ctx->device);
     cudaStream_t s = ctx->stream;
@@ -1802,7 +1989,7 @@ int fmv_matvec_partitioned_2d(fmv_ctx* ctx, const fmv_op* op, int kind, const ch
     const bool root = fwd ? ctx->ri == 0 : ctx->cj == 0;
     void* bcomm = fwd ? ctx->col_comm : ctx->row_comm;
     void* rcomm = fwd ? ctx->row_comm : ctx->col_comm;
-    const int bsize = fwd ? ctx->pr : ctx->pc, rsize = fwd ? ctx->pc : ctx->pr;
+    const int rsize = fwd ? ctx->pc : ctx->pr, rrank = fwd ? ctx->cj : ctx->ri;
     if (root && !in) fail(FMV_EINVAL, "fmv_matvec_partitioned_2d: null input on a root rank");
     const double* din = in;
     double* dout = out;
@@ -1813,11 +2000,11 @@ int fmv_matvec_partitioned_2d(fmv_ctx* ctx, const fmv_op* op, int kind, const ch
       din = static_cast<const double*>(ctx->io_in.p);
       dout = static_cast<double*>(ctx->io_out.p);
     }
-    const auto pay = bcast_payload(ctx, bcomm, bsize, root, din, (long)n_in, p[0]);
-    pipeline(ctx, op, kind, p, pay.first, pay.second, dout);
-    allreduce_prec(ctx, rcomm, rsize, dout, (long)n_out, p[4]);
+    const auto pay = bcast_payload(ctx, bcomm, root, din, (long)n_in, p[0]);
+    pipeline(ctx, op, kind, p, pay.first, p[0] == PD && !bcomm ? -1 : pay.second, dout);
+    reduce_partials(ctx, rcomm, rsize, rrank, dout, (long)n_out, p[4]);
     if (!io_on_device) CK(cudaMemcpyAsync(out, dout, n_out * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    comm_sync(ctx);
   });
 }
 
@@ -1840,6 +2027,7 @@ int fmv_graph_create(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, 
   fmv_graph* g = nullptr;
   const int rc = guarded([&] {
     if (!ctx || !op || !d_in || !d_out || !out) fail(FMV_EINVAL, "fmv_graph_create: null argument");
+    check_same_device(ctx, op);
     if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
     const auto p = parse_cfg(cfg);
     DeviceGuard dg(ctx->device);

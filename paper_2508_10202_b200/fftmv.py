@@ -409,16 +409,37 @@ def _check_input(op: SpectralOperator, v: BlockVector, forward: bool) -> None:
         v.validate()
 
 
-def run_pipeline(op: SpectralOperator, kind: MatvecKind, inp, cfg="ddddd", ctx: Optional[Context] = None):
+_PAYLOAD_DTYPES = {"d": np.float64, "s": np.float32, "h": np.float16}
+
+
+def run_pipeline(op: SpectralOperator, kind: MatvecKind, inp, cfg="ddddd", ctx: Optional[Context] = None,
+                 timings: bool = True, payload: Optional[str] = None):
     """matvec.hpp:233-289: returns (output, PhaseTimings). ``inp`` is a float64
-    numpy array (host I/O) or a CUDA float64 torch tensor (device I/O)."""
+    numpy array (host I/O) or a CUDA float64 torch tensor (device I/O).
+
+    Host I/O always runs the overlapped schedule (input / output copies in
+    column chunks beside the SBGEMV); ``timings=False`` skips the CUDA-event
+    bookkeeping (``times = NULL`` at the C ABI) and returns zero timings.
+    ``payload`` = 'd' / 's' / 'h': ``inp`` is a broadcast payload already
+    rounded to cfg[0] and stored in that precision (float64 / float32 /
+    float16 numpy array, matvec.hpp:240 ``payload``; partition.hpp:198-212)."""
     ctx = ctx or op.ctx
     fwd = kind == MatvecKind.Forward
     n_in = (op.dims.n_m if fwd else op.dims.n_d) * op.dims.n_t
     n_out = (op.dims.n_d if fwd else op.dims.n_m) * op.dims.n_t
     cs = _cfg_str(cfg).encode()
     t = _capi.PhaseTimesC()
-    if _is_cuda_tensor(inp):
+    tp = ctypes.byref(t) if timings else None
+    if payload is not None:
+        if payload not in _PAYLOAD_DTYPES:
+            raise ValueError("run_pipeline: payload precision must be 'd', 's' or 'h'")
+        x = np.ascontiguousarray(inp, dtype=_PAYLOAD_DTYPES[payload]).reshape(-1)
+        if x.size != n_in:
+            raise ValueError("matvec: input length does not match operator dims")
+        out = np.empty(n_out, dtype=np.float64)
+        check(lib().fmv_matvec_payload(ctx.handle, op.handle, int(kind), cs, payload.encode(), x.ctypes.data,
+                                       out.ctypes.data, 0, tp))
+    elif _is_cuda_tensor(inp):
         import torch
 
         if inp.dtype != torch.float64 or inp.numel() != n_in:
@@ -427,33 +448,35 @@ def run_pipeline(op: SpectralOperator, kind: MatvecKind, inp, cfg="ddddd", ctx: 
         out = torch.empty(n_out, dtype=torch.float64, device=x.device)
         torch.cuda.current_stream(x.device).synchronize()
         check(lib().fmv_matvec(ctx.handle, op.handle, int(kind), cs, ctypes.c_void_p(x.data_ptr()),
-                               ctypes.c_void_p(out.data_ptr()), 1, ctypes.byref(t)))
+                               ctypes.c_void_p(out.data_ptr()), 1, tp))
     else:
         x = np.ascontiguousarray(inp, dtype=np.float64).reshape(-1)
         if x.size != n_in:
             raise ValueError("matvec: input length does not match operator dims")
         out = np.empty(n_out, dtype=np.float64)
-        check(lib().fmv_matvec(ctx.handle, op.handle, int(kind), cs, x.ctypes.data, out.ctypes.data, 0,
-                               ctypes.byref(t)))
+        check(lib().fmv_matvec(ctx.handle, op.handle, int(kind), cs, x.ctypes.data, out.ctypes.data, 0, tp))
     return out, PhaseTimings(list(t.phase_s), t.total_s)
 
 
-def forward_matvec(op: SpectralOperator, m: BlockVector, cfg="ddddd", tiling=None) -> MatvecResult:
+def forward_matvec(op: SpectralOperator, m: BlockVector, cfg="ddddd", tiling=None,
+                   timings: bool = True) -> MatvecResult:
     """matvec.hpp:305-310: d = F m. ``tiling`` (TilingParams) is accepted for
-    signature parity and ignored: the B200 kernels pick their own tiles."""
+    signature parity and ignored: the B200 kernels pick their own tiles.
+    ``timings=False``: no PhaseTimings bookkeeping (zeros returned)."""
     if not isinstance(m, BlockVector):
         m = BlockVector.time_double(op.dims.n_m, op.dims.n_t, m)
     _check_input(op, m, True)
-    out, t = run_pipeline(op, MatvecKind.Forward, m.data, cfg)
+    out, t = run_pipeline(op, MatvecKind.Forward, m.data, cfg, timings=timings)
     return MatvecResult(BlockVector.time_double(op.dims.n_d, op.dims.n_t, out), t)
 
 
-def adjoint_matvec(op: SpectralOperator, d: BlockVector, cfg="ddddd", tiling=None) -> MatvecResult:
+def adjoint_matvec(op: SpectralOperator, d: BlockVector, cfg="ddddd", tiling=None,
+                   timings: bool = True) -> MatvecResult:
     """matvec.hpp:313-318: m = F* d."""
     if not isinstance(d, BlockVector):
         d = BlockVector.time_double(op.dims.n_d, op.dims.n_t, d)
     _check_input(op, d, False)
-    out, t = run_pipeline(op, MatvecKind.Adjoint, d.data, cfg)
+    out, t = run_pipeline(op, MatvecKind.Adjoint, d.data, cfg, timings=timings)
     return MatvecResult(BlockVector.time_double(op.dims.n_m, op.dims.n_t, out), t)
 
 

@@ -173,11 +173,11 @@ def adjoint_matvec_partitioned(pop: PartitionedOperator, d, cfg="ddddd") -> Part
     nt = pop.dims.n_t
     if d.size != pop.dims.n_d * nt:
         raise ValueError("partitioned matvec: input extents do not match dims")
-    payload = round_to(d, c[0])
+    payload = round_to(d, c[0])  # one cast (partition.hpp:198-203), stored in cfg[0]'s own type
     total = PhaseTimings()
     out = np.empty(pop.dims.n_m * nt)
     for (lo, hi), op in zip(pop.grid.shard_ranges, pop.workers):
-        shard, t = run_pipeline(op, MatvecKind.Adjoint, payload, _payload_cfg(c))
+        shard, t = run_pipeline(op, MatvecKind.Adjoint, payload, c, payload=c[0])
         total += t
         out[lo * nt:hi * nt] = shard
     return PartitionedResult(BlockVector.time_double(pop.dims.n_m, nt, out), total)
@@ -275,16 +275,22 @@ class DistributedMatvec:
             torch.cuda.current_stream(x.device).synchronize()
             check(lib().fmv_matvec_partitioned(self.ctx.handle, self.shard.handle, int(kind), c.encode(),
                                                ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), 1,
-                                               ctypes.byref(t)))
+                                               ctypes.byref(t) if times else None))
         else:
             out = np.empty(n_out)
             xin = None if x is None else np.ascontiguousarray(x, dtype=np.float64)
             check(lib().fmv_matvec_partitioned(self.ctx.handle, self.shard.handle, int(kind), c.encode(),
                                                None if xin is None else xin.ctypes.data, out.ctypes.data, 0,
-                                               ctypes.byref(t)))
+                                               ctypes.byref(t) if times else None))
         if times:
             return out, PhaseTimings(list(t.phase_s), t.total_s)
         return out
+
+    def comm_size(self) -> tuple:
+        """(nranks, rank) of the library's live communicator (native transport)."""
+        n, r = ctypes.c_int(), ctypes.c_int()
+        check(lib().fmv_comm_size(self.ctx.handle, ctypes.byref(n), ctypes.byref(r)))
+        return n.value, r.value
 
     def close(self):
         if self.transport == "native" and self.ctx is not None:
