@@ -9,14 +9,26 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC -Xcompiler -Wall --
 PKG := paper_2508_10202_b200
 # nlohmann/json.hpp (sweep.hpp includes it unconditionally, as the reference's sweep.hpp:20 does)
 JSON_INC := $(shell python -c "import sysconfig;print(sysconfig.get_paths()['purelib'])")/include/cudnn_frontend/thirdparty/nlohmann
-SRC := $(wildcard $(PKG)/csrc/*.cu) $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.cpp) include/fftmv_cuda.h
 
 all: lib oracle cpp cli stub
 
 lib: $(PKG)/libfftmv_cuda.so
 
-$(PKG)/libfftmv_cuda.so: $(SRC)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(PKG)/csrc/fmv_capi.cu $(PKG)/csrc/fmv_host.cpp -ldl -lcudart 2> build_ptxas.log || (cat build_ptxas.log; false)
+# one object per translation unit so `make -j` compiles them in parallel
+OBJS := build/obj/fmv_capi.o build/obj/fmv_fft_launch.o build/obj/fmv_gemv_launch.o build/obj/fmv_host.o
+HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/fftmv_cuda.h
+
+$(PKG)/libfftmv_cuda.so: $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl -lcudart
+	@cat build/obj/*.ptxas.log > build_ptxas.log
+
+build/obj/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p build/obj
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/obj/$*.ptxas.log || (cat build/obj/$*.ptxas.log; false)
+
+build/obj/fmv_host.o: $(PKG)/csrc/fmv_host.cpp include/fftmv_cuda.h
+	@mkdir -p build/obj
+	g++ -std=c++20 -O2 -fPIC -Wall -c -o $@ $<
 
 oracle:
 	$(MAKE) -C oracle all

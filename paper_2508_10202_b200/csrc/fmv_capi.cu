@@ -1,289 +1,23 @@
 // fmv_capi.cu -- host runtime behind include/fftmv_cuda.h.
 //
 // Owns device memory for spectral operators, per-context workspaces and
-// streams, launches the fused sm_100a kernels of the five-phase pipeline
-// (matvec.hpp:233-289) and the 1 x p NCCL partition (partition.hpp:141-217).
-// No CPU fallback exists: every compute entry point launches CUDA kernels
-// and fails loudly on any CUDA error.
+// streams, runs the fused sm_100a kernels of the five-phase pipeline
+// (matvec.hpp:233-289; FFT dispatch in fmv_fft_launch.cu, SBGEMV dispatch in
+// fmv_gemv_launch.cu) and the 1 x p / 2-D NCCL partition
+// (partition.hpp:141-217). No CPU fallback exists: every compute entry point
+// launches CUDA kernels and fails loudly on any CUDA error.
 #include <dlfcn.h>
 
-#include <algorithm>
-#include <array>
-#include <atomic>
-#include <chrono>
-#include <cmath>
-#include <cstdio>
-#include <cstring>
-#include <map>
-#include <memory>
-#include <mutex>
-#include <stdexcept>
-#include <string>
-#include <thread>
-#include <tuple>
-#include <utility>
-#include <vector>
+#include "fmv_runtime.cuh"
 
-#include "../../include/fftmv_cuda.h"
-#include "fmv_common.cuh"
-#include "fmv_fft.cuh"
-#include "fmv_sbgemv.cuh"
-#include "fmv_sbgemm_block.cuh"
-
-using namespace fmv;
-
-// ======================================================================
-// errors
-// ======================================================================
-namespace {
+namespace fmv {
+namespace rt {
 thread_local std::string g_err;
-
-struct FmvError {
-  int code;
-  std::string msg;
-};
-[[noreturn]] void fail(int code, const std::string& m) { throw FmvError{code, m}; }
-
-void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) {
-    (void)cudaGetLastError();
-    fail(e == cudaErrorMemoryAllocation ? FMV_ENOMEM : FMV_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
-  }
-}
-#define CK(x) ck((x), #x)
-
-template <class F>
-int guarded(F&& f) {
-  try {
-    f();
-    return FMV_OK;
-  } catch (const FmvError& e) {
-    g_err = e.msg;
-    return e.code;
-  } catch (const std::bad_alloc&) {
-    g_err = "host allocation failed";
-    return FMV_ENOMEM;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return FMV_ECUDA;
-  }
-}
-
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    CK(cudaGetDevice(&prev));
-    if (prev != dev) CK(cudaSetDevice(dev));
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
-  }
-};
-
 std::atomic<uint64_t> g_casts{0};
+}  // namespace rt
+}  // namespace fmv
 
-int prec_of(char c) {
-  switch (c) {
-    case 'd': return PD;
-    case 's': return PS;
-    case 'h': return PH;
-    default: fail(FMV_EINVAL, std::string("precision config: invalid character '") + c + "'");
-  }
-}
-
-// config.hpp:36-51 plus the 'h' extension rules.
-std::array<int, 5> parse_cfg(const char* cfg) {
-  if (!cfg) fail(FMV_EINVAL, "precision config is null");
-  const size_t len = strnlen(cfg, 16);
-  if (len != 5)
-    fail(FMV_EINVAL, "precision config must be exactly 5 characters, got " + std::to_string(len));
-  std::array<int, 5> p{};
-  for (int i = 0; i < 5; ++i) {
-    if (cfg[i] != 'd' && cfg[i] != 's' && cfg[i] != 'h')
-      fail(FMV_EINVAL, std::string("precision config: invalid character '") + cfg[i] + "' at position " +
-                           std::to_string(i + 1) + " (expected 'd', 's' or 'h')");
-    p[i] = prec_of(cfg[i]);
-  }
-  if (p[1] == PH || p[3] == PH)
-    fail(FMV_EINVAL, "precision config: fp16 ('h') is supported for phases 1, 3 and 5 only (pad, sbgemv, unpad)");
-  return p;
-}
-
-// Logical cast passes of run_pipeline (matvec.hpp:88, :121-125, :163, :189-190).
-uint64_t count_casts(const std::array<int, 5>& p, bool payload) {
-  uint64_t n = 0;
-  if (!payload && p[0] != PD) ++n;
-  if (p[0] != p[1]) ++n;
-  if (p[1] != p[2]) ++n;
-  if (p[2] != p[3]) ++n;
-  if (p[3] != p[4]) ++n;
-  if (p[4] != PD) ++n;
-  return n;
-}
-
-size_t esize(int prec) { return prec == PD ? 16 : prec == PS ? 8 : 4; }
-
-// ======================================================================
-// FFT geometry + twiddle tables (per device, per L, per precision)
-// ======================================================================
-FftGeom make_geom(int Nt, int nout) {
-  FftGeom g{};
-  g.N = Nt;
-  g.L = 2 * Nt;
-  g.n_div = FastDiv((uint32_t)Nt);
-  g.nb_div = FastDiv((uint32_t)Nt + 1);
-  g.nout_div = FastDiv((uint32_t)nout);
-  int n = Nt;
-  while (n > 1) {
-    int r;
-    if (n % 8 == 0 && n != 16) r = 8;  // 16 = 4*4 beats 8*2
-    else if (n % 4 == 0) r = 4;
-    else if (n % 2 == 0) r = 2;
-    else if (n % 5 == 0) r = 5;
-    else if (n % 3 == 0) r = 3;
-    else {
-      r = 7;
-      while (n % r) r += 2;  // smallest remaining odd prime factor >= 7
-    }
-    if (g.nst >= kMaxStages) fail(FMV_EUNSUPPORTED, "FFT: too many stages");
-    g.radix[g.nst++] = r;
-    n /= r;
-  }
-  int Ns = 1;
-  for (int st = 0; st < g.nst; ++st) {
-    g.nr_div[st] = FastDiv((uint32_t)(Nt / g.radix[st]));
-    g.ns_div[st] = FastDiv((uint32_t)Ns);
-    g.span_div[st] = FastDiv((uint32_t)(Ns * g.radix[st]));
-    Ns *= g.radix[st];
-  }
-  return g;
-}
-
-struct TwiddleCache {
-  std::mutex mu;
-  // (device, L, prec, RX) -> device table; RX = 0: the base table
-  // exp(-2*pi*i*m/L), m < L; RX > 1: the base table followed by one table per
-  // register-FFT pass p = 2..NP (Ns = RX^(p-1)) laid out [q*Ns + k] =
-  // base[q*k*L/(Ns*RX)], so a warp's twiddle read for fixed q is contiguous
-  // in k (k_r2c_reg / k_c2r_reg); the values are bitwise the base table's.
-  std::map<std::tuple<int, int, int, int>, void*> tabs;
-  ~TwiddleCache() {}  // tables live for the process (like the reference's plan cache, fft.hpp:152-164)
-  const void* get(int dev, int L, int prec, int RX = 0) {
-    std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(dev, L, prec, RX);
-    auto it = tabs.find(key);
-    if (it != tabs.end()) return it->second;
-    // exp(-2*pi*i*m/L), long double, exact at multiples of pi/2
-    std::vector<double> re(L), im(L);
-    const long double pi = 3.141592653589793238462643383279502884L;
-    for (int m = 0; m < L; ++m) {
-      long double c, s;
-      if ((4L * m) % L == 0) {
-        const int q = (int)((4L * m) / L);
-        const int cs[4] = {1, 0, -1, 0}, sn[4] = {0, -1, 0, 1};
-        c = cs[q];
-        s = sn[q];
-      } else {
-        const long double a = -2.0L * pi * (long double)m / (long double)L;
-        c = cosl(a);
-        s = sinl(a);
-      }
-      re[m] = (double)c;
-      im[m] = (double)s;
-      if (prec == PS) {
-        re[m] = (double)(float)c;
-        im[m] = (double)(float)s;
-      }
-    }
-    if (RX > 1) {
-      const int N = L / 2;
-      for (int Ns = RX; Ns < N; Ns *= RX) {
-        for (int q = 0; q < RX; ++q)
-          for (int k = 0; k < Ns; ++k) {
-            const int m = q * k * (L / (Ns * RX));
-            re.push_back(re[m]);
-            im.push_back(im[m]);
-          }
-      }
-    }
-    L = (int)re.size();
-    void* d = nullptr;
-    if (prec == PD) {
-      std::vector<double2> h(L);
-      for (int m = 0; m < L; ++m) h[m] = make_double2(re[m], im[m]);
-      CK(cudaMalloc(&d, L * sizeof(double2)));
-      CK(cudaMemcpy(d, h.data(), L * sizeof(double2), cudaMemcpyHostToDevice));
-    } else {
-      std::vector<float2> h(L);
-      for (int m = 0; m < L; ++m) h[m] = make_float2((float)re[m], (float)im[m]);
-      CK(cudaMalloc(&d, L * sizeof(float2)));
-      CK(cudaMemcpy(d, h.data(), L * sizeof(float2), cudaMemcpyHostToDevice));
-    }
-    tabs[key] = d;
-    return d;
-  }
-};
-TwiddleCache& twiddles() {
-  static TwiddleCache* c = new TwiddleCache;  // intentionally leaked: outlives static destructors
-  return *c;
-}
-
-// Tunables (env overridable for on-GPU sweeps): SBGEMV stage bytes / ring
-// depth / CTAs per SM, FFT shared-memory budget.
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
-
-// Kernel attributes are per device (cudaFuncSetAttribute applies to the
-// current one), so both caches are keyed by (device, function).
-int cur_device() {
-  int d = 0;
-  CK(cudaGetDevice(&d));
-  return d;
-}
-
-// Raise a kernel's dynamic shared-memory cap once per (device, function, size).
-void prep_smem(const void* fn, size_t bytes) {
-  static std::mutex mu;
-  static std::map<std::pair<int, const void*>, size_t> set;
-  if (bytes <= 48 * 1024) return;
-  const int dev = cur_device();
-  std::lock_guard<std::mutex> lk(mu);
-  size_t& cur = set[{dev, fn}];
-  if (bytes > cur) {
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    cur = bytes;
-  }
-}
-
-// Ask for the maximum shared-memory carveout once per (device, function), so
-// more CTAs of the register FFT kernels fit per SM.
-void prep_carveout(const void* fn) {
-  static std::mutex mu;
-  static std::map<std::pair<int, const void*>, bool> set;
-  const int dev = cur_device();
-  std::lock_guard<std::mutex> lk(mu);
-  bool& done = set[{dev, fn}];
-  if (!done) {
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    done = true;
-  }
-}
-
-int sm_count(int dev) {
-  static std::mutex mu;
-  static std::map<int, int> cache;
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find(dev);
-  if (it != cache.end()) return it->second;
-  int n = 0;
-  CK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-  cache[dev] = n;
-  return n;
-}
-
+namespace {
 // ======================================================================
 // NCCL (dlopen'ed on first use: only the partitioned path needs it)
 // ======================================================================
@@ -352,565 +86,12 @@ constexpr int kNcclHalf = 6, kNcclFloat = 7, kNcclDouble = 8, kNcclSum = 0;
 }  // namespace
 
 // ======================================================================
-// handles
+// pipeline
 // ======================================================================
-struct DevBuf {
-  void* p = nullptr;
-  size_t n = 0;
-  void ensure(size_t bytes) {
-    if (bytes <= n) return;
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-    CK(cudaMalloc(&p, bytes));
-    n = bytes;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-  }
-};
-
-struct ProfRec {
-  int cls;
-  cudaEvent_t a, b;
-};
-
-struct fmv_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  DevBuf x, y, yacc, io_in, io_out, partials, counters, payload, red;
-  cudaStream_t copy_stream = nullptr;
-  cudaEvent_t cev[34] = {};
-  size_t counters_len = 0;
-  uint64_t launches = 0;
-  bool profiling = false;
-  std::vector<ProfRec> prof;
-  std::vector<cudaEvent_t> ev_pool;
-  double prof_ms[5] = {0, 0, 0, 0, 0};
-  uint64_t prof_n[5] = {0, 0, 0, 0, 0};
-  void* comm = nullptr;
-  int nranks = 1, rank = 0;
-  // 2-D pr x pc grid (fmv_comm_init_2d): rank = ri * pc + cj; row_comm joins
-  // the pc ranks of grid row ri, col_comm the pr ranks of grid column cj.
-  void* row_comm = nullptr;
-  void* col_comm = nullptr;
-  int pr = 1, pc = 1, ri = 0, cj = 0;
-  cudaEvent_t te[8] = {};
-  // PhaseTimings of one blocking matvec (fmv_matvec with times != NULL):
-  // every kernel launch, copy and collective records a CUDA-event pair on the
-  // stream it runs on, tagged with the reference phase it belongs to.
-  bool phase_timing = false;
-  struct PhaseRec {
-    int phase;
-    cudaEvent_t a, b;
-  };
-  std::vector<PhaseRec> phase_recs;
-
-  cudaEvent_t ev() {
-    if (!ev_pool.empty()) {
-      cudaEvent_t e = ev_pool.back();
-      ev_pool.pop_back();
-      return e;
-    }
-    cudaEvent_t e;
-    CK(cudaEventCreate(&e));
-    return e;
-  }
-  // Zeroed ticket counters for the SBGEMV-N cross-CTA reduction.
-  unsigned* tickets(size_t nbatch) {
-    if (nbatch > counters_len) {
-      counters.ensure(nbatch * sizeof(unsigned));
-      CK(cudaMemsetAsync(counters.p, 0, nbatch * sizeof(unsigned), stream));
-      counters_len = nbatch;
-    }
-    return static_cast<unsigned*>(counters.p);
-  }
-};
-
-struct fmv_op {
-  int device = 0;
-  size_t nm = 0, nd = 0, nt = 0;
-  void* bins_d = nullptr;  // double2, lda = nd
-  // fp32 / fp16 copies, published (release) only after their cast kernel has
-  // finished and lda_s / lda_h are set; readers load them with acquire.
-  std::atomic<void*> bins_s{nullptr};  // float2, lda = lda_s
-  std::atomic<void*> bins_h{nullptr};  // __half2, lda = lda_h
-  size_t lda_s = 0, lda_h = 0;
-  std::mutex mu;
-  size_t nb() const { return nt + 1; }
-};
-
 namespace {
-
-// ---------------------------------------------------------------- launch --
-// Reference phase (matvec.hpp:42-51) a kernel class is charged to: r2c ->
-// [1] fft (pad + convert + reorder fused in), SBGEMV -> [2], c2r -> [3] ifft
-// (reorder + unpad fused in). Class 4 (cast kernels) is charged explicitly by
-// the caller; a first fp32/fp16 operator materialization inside a matvec goes
-// to [2] like the reference's ensure_single inside gemv_stage.
-constexpr int kPhaseOfClass[5] = {1, 2, 2, 3, 2};
-
-// Run fn (which enqueues work on `s`) inside a CUDA-event span of `phase`
-// when the context is collecting PhaseTimings.
-template <class Fn>
-void phase_span(fmv_ctx* ctx, cudaStream_t s, int phase, Fn&& fn) {
-  if (!ctx->phase_timing) {
-    fn();
-    return;
-  }
-  fmv_ctx::PhaseRec r{phase, ctx->ev(), ctx->ev()};
-  CK(cudaEventRecord(r.a, s));
-  fn();
-  CK(cudaEventRecord(r.b, s));
-  ctx->phase_recs.push_back(r);
-}
-
-template <class Fn>
-void launch(fmv_ctx* ctx, int cls, Fn&& fn, int phase = -1) {
-  ProfRec r{cls, nullptr, nullptr};
-  if (ctx->profiling) {
-    r.a = ctx->ev();
-    r.b = ctx->ev();
-    CK(cudaEventRecord(r.a, ctx->stream));
-  }
-  phase_span(ctx, ctx->stream, phase >= 0 ? phase : kPhaseOfClass[cls], [&] {
-    fn();
-    CK(cudaGetLastError());
-  });
-  ++ctx->launches;
-  if (ctx->profiling) {
-    CK(cudaEventRecord(r.b, ctx->stream));
-    ctx->prof.push_back(r);
-  }
-}
-
-// cudaMemcpyAsync charged to a phase ([0] for input copies, [4] for output).
-void copy_async(fmv_ctx* ctx, int phase, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
-                cudaStream_t s) {
-  phase_span(ctx, s, phase, [&] { CK(cudaMemcpyAsync(dst, src, bytes, kind, s)); });
-}
-
-// Collects the phase spans of one matvec: sums the busy time per phase
-// (spans of one phase never overlap each other; spans of different phases
-// may, on the overlapped host-I/O path) and the wall time from `t0` to `t1`
-// (events recorded on the matvec stream around everything). Call after the
-// stream has been synchronized.
-void collect_phase_times(fmv_ctx* ctx, cudaEvent_t t0, cudaEvent_t t1, fmv_phase_times* out) {
-  double ms[5] = {0, 0, 0, 0, 0};
-  for (auto& r : ctx->phase_recs) {
-    float v = 0.f;
-    CK(cudaEventElapsedTime(&v, r.a, r.b));
-    ms[r.phase] += v;
-    ctx->ev_pool.push_back(r.a);
-    ctx->ev_pool.push_back(r.b);
-  }
-  ctx->phase_recs.clear();
-  float tot = 0.f;
-  CK(cudaEventElapsedTime(&tot, t0, t1));
-  for (int i = 0; i < 5; ++i) out->phase_s[i] = ms[i] * 1e-3;
-  out->total_s = tot * 1e-3;
-}
-
-// Turns per-call phase timing on for a scope (and drops the records of a
-// call that failed part-way).
-struct PhaseTimingScope {
-  fmv_ctx* ctx;
-  PhaseTimingScope(fmv_ctx* c, bool on) : ctx(c) {
-    for (auto& r : ctx->phase_recs) {
-      ctx->ev_pool.push_back(r.a);
-      ctx->ev_pool.push_back(r.b);
-    }
-    ctx->phase_recs.clear();
-    ctx->phase_timing = on;
-  }
-  ~PhaseTimingScope() { ctx->phase_timing = false; }
-};
-
-// Launch with programmatic dependent launch allowed (FMV_PDL=0 disables).
-template <class... KArgs, class... Args>
-void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
-  static const bool on = env_int("FMV_PDL", 1) != 0;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = on ? 1 : 0;
-  CK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
-}
-
-// log2 of the series per CTA (a power of two, <= 16) for a 64 KB smem budget.
-int fft_lg_series_per_cta(int N, size_t celem) {
-  const size_t per = 2 * (size_t)(N + 1) * celem;
-  if (per > 200 * 1024)
-    fail(FMV_EUNSUPPORTED, "FFT: n_t = " + std::to_string(N) + " exceeds the shared-memory FFT capacity");
-  const size_t budget = (size_t)env_int("FMV_FFT_SMEM_BUDGET", 64 * 1024);
-  int lg = 0;
-  while (lg < 4 && per * ((size_t)2 << lg) <= budget) ++lg;
-  return lg;
-}
-
-// Register-resident FFT kernels (fmv_fft.cuh k_r2c_reg / k_c2r_reg) cover
-// N = 1000 (10^3) and N = 100 (10^2), SOTI <-> TOSI; everything else (and
-// FMV_FFT_LEGACY=1) uses the general mixed-radix kernels.
-#ifndef FMV_FFT_S64
-#define FMV_FFT_S64 2  // fp64 Nt = 1000 series per CTA of the register FFT kernels
-#endif
-bool fft_reg_ok(int N) {
-  return (N == 1000 || N == 100) && env_int("FMV_FFT_LEGACY", 0) == 0;
-}
-
-template <int C0, int C1, int C2, class Tin, int RX, int NP, int S>
-void r2c_reg_launch(fmv_ctx* ctx, const Tin* in, long in_ss, long nseries, int nvalid, void* out, long out_ks) {
-  using R = typename PT<C1>::real;
-  using C = typename CT<R>::c;
-  const int N = RegPlan<RX, NP>::N;
-  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, 2 * N, C1, RX));
-  bool vec = (in_ss % 2 == 0) && (nvalid % 2 == 0);
-  if constexpr (sizeof(Tin) == 8) vec = vec && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
-  else if constexpr (sizeof(Tin) == 4) vec = vec && (reinterpret_cast<uintptr_t>(in) & 7) == 0;
-  else vec = false;
-  const long grid = (nseries + S - 1) / S;
-  constexpr size_t smem = r2c_reg_smem<C, RX, NP, S>();
-  prep_smem((const void*)k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>, smem);
-  prep_carveout((const void*)k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>);
-  launch(ctx, 0, [&] {
-    launch_pdl(k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>, dim3((unsigned)grid), dim3(S * RegPlan<RX, NP>::NR), smem,
-               ctx->stream, in, in_ss, nseries, nvalid, vec, static_cast<typename PT<C2>::cplx*>(out), out_ks, tw);
-  });
-}
-
-template <int C0, int C1, int C2, class Tin>
-void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, int N, int nvalid, void* out,
-           long out_ks, long out_ss) {
-  using R = typename PT<C1>::real;
-  using C = typename CT<R>::c;
-  constexpr bool tin_ok = sizeof(Tin) == 8 || (sizeof(Tin) == 4 && C0 == PS) || (sizeof(Tin) == 2 && C0 == PH);
-  if constexpr (tin_ok) {
-    if (in_ts == 1 && out_ss == 1 && fft_reg_ok(N)) {
-      constexpr bool f64 = sizeof(R) == 8;
-      // (fp64: one series per CTA for small batches -- more CTAs for the 100-series transforms)
-      if (N == 1000 && f64 && nseries < 1024)
-        r2c_reg_launch<C0, C1, C2, Tin, 10, 3, 1>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
-      else if (N == 1000)
-        r2c_reg_launch<C0, C1, C2, Tin, 10, 3, f64 ? FMV_FFT_S64 : 4>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
-      else
-        r2c_reg_launch<C0, C1, C2, Tin, 10, 2, f64 ? 16 : 32>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
-      return;
-    }
-  }
-  const FftGeom g = make_geom(N, nvalid);
-  const int lgS = fft_lg_series_per_cta(g.N, sizeof(C));
-  const int S = 1 << lgS;
-  const size_t smem = 2 * (size_t)S * (g.N + 1) * sizeof(C);
-  auto kern = k_r2c<C0, C1, C2, Tin>;
-  prep_smem((const void*)kern, smem);
-  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, g.L, C1));
-  const long grid = (nseries + S - 1) / S;
-  launch(ctx, 0, [&] {
-    kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(in, in_ss, in_ts, nseries, nvalid,
-                                                     static_cast<typename PT<C2>::cplx*>(out), out_ks, out_ss, g, tw, lgS);
-  });
-}
-
-// N = L/2 (complex FFT length); nvalid = input samples per series (Nt for
-// the zero-padded matvec path, L for a plain transform).
-template <class Tin>
-void r2c_dispatch(fmv_ctx* ctx, int c0, int c1, int c2, const Tin* in, long in_ss, long in_ts, long nseries, int N,
-                  int nvalid, void* out, long out_ks, long out_ss) {
-#define R2C_CASE(A, B, C)                                                                      \
-  if (c0 == A && c1 == B && c2 == C) {                                                         \
-    r2c_t<A, B, C, Tin>(ctx, in, in_ss, in_ts, nseries, N, nvalid, out, out_ks, out_ss);       \
-    return;                                                                                    \
-  }
-  R2C_CASE(PD, PD, PD) R2C_CASE(PD, PD, PS) R2C_CASE(PD, PD, PH)
-  R2C_CASE(PD, PS, PD) R2C_CASE(PD, PS, PS) R2C_CASE(PD, PS, PH)
-  R2C_CASE(PS, PD, PD) R2C_CASE(PS, PD, PS) R2C_CASE(PS, PD, PH)
-  R2C_CASE(PS, PS, PD) R2C_CASE(PS, PS, PS) R2C_CASE(PS, PS, PH)
-  R2C_CASE(PH, PD, PD) R2C_CASE(PH, PD, PS) R2C_CASE(PH, PD, PH)
-  R2C_CASE(PH, PS, PD) R2C_CASE(PH, PS, PS) R2C_CASE(PH, PS, PH)
-#undef R2C_CASE
-  fail(FMV_EINVAL, "r2c: unsupported precision combination");
-}
-
-template <int C3, int C4, class Tout, int RX, int NP, int S>
-void c2r_reg_launch(fmv_ctx* ctx, const void* in, long in_ks, long nseries, int nout, Tout* out, long out_ss) {
-  using C = typename PT<C3>::cplx;
-  const int N = RegPlan<RX, NP>::N;
-  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, 2 * N, C3, RX));
-  const bool vec = sizeof(Tout) == 8 && (out_ss % 2 == 0) && (nout % 2 == 0) &&
-                   (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-  const long grid = (nseries + S - 1) / S;
-  using Cr = typename CT<typename PT<C3>::real>::c;
-  constexpr size_t smem = c2r_reg_smem<Cr, RX, NP, S>();
-  prep_smem((const void*)k_c2r_reg<C3, C4, Tout, RX, NP, S>, smem);
-  prep_carveout((const void*)k_c2r_reg<C3, C4, Tout, RX, NP, S>);
-  launch(ctx, 3, [&] {
-    launch_pdl(k_c2r_reg<C3, C4, Tout, RX, NP, S>, dim3((unsigned)grid), dim3(S * RegPlan<RX, NP>::NR), smem,
-               ctx->stream, static_cast<const C*>(in), in_ks, nseries, nout, vec, out, out_ss, tw);
-  });
-}
-
-template <int C3, int C4, class Tout>
-void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, int N, int nout, Tout* out,
-           long out_ss) {
-  using C = typename PT<C3>::cplx;
-  if (in_ss == 1 && fft_reg_ok(N)) {
-    constexpr bool f64 = C3 == PD;
-    if (N == 1000)
-    {
-      // fp32: 8 series per CTA for the big (Nm-series) transform, 2 for the small
-      // one (tools/tune_fft.py at C2: 45.5 -> 39.3 us, and 10.5 us)
-      if constexpr (f64) {
-        if (nseries < 1024) c2r_reg_launch<C3, C4, Tout, 10, 3, 1>(ctx, in, in_ks, nseries, nout, out, out_ss);
-        else c2r_reg_launch<C3, C4, Tout, 10, 3, FMV_FFT_S64>(ctx, in, in_ks, nseries, nout, out, out_ss);
-      }
-      else if (nseries >= 1024) c2r_reg_launch<C3, C4, Tout, 10, 3, 8>(ctx, in, in_ks, nseries, nout, out, out_ss);
-      else c2r_reg_launch<C3, C4, Tout, 10, 3, 2>(ctx, in, in_ks, nseries, nout, out, out_ss);
-    }
-    else
-      c2r_reg_launch<C3, C4, Tout, 10, 2, f64 ? 16 : 32>(ctx, in, in_ks, nseries, nout, out, out_ss);
-    return;
-  }
-  const FftGeom g = make_geom(N, nout);
-  const int lgS = fft_lg_series_per_cta(g.N, sizeof(C));
-  const int S = 1 << lgS;
-  const size_t smem = 2 * (size_t)S * (g.N + 1) * sizeof(C);
-  auto kern = k_c2r<C3, C4, Tout>;
-  prep_smem((const void*)kern, smem);
-  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, g.L, C3));
-  const long grid = (nseries + S - 1) / S;
-  launch(ctx, 3, [&] {
-    kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(static_cast<const C*>(in), in_ks, in_ss, nseries, nout, out,
-                                                     out_ss, g, tw, lgS);
-  });
-}
-
-void c2r_dispatch(fmv_ctx* ctx, int c3, int c4, const void* in, long in_ks, long in_ss, long nseries, int N,
-                  int nout, double* out, long out_ss) {
-#define C2R_CASE(A, B)                                                              \
-  if (c3 == A && c4 == B) {                                                         \
-    c2r_t<A, B, double>(ctx, in, in_ks, in_ss, nseries, N, nout, out, out_ss);      \
-    return;                                                                         \
-  }
-  C2R_CASE(PD, PD) C2R_CASE(PD, PS) C2R_CASE(PD, PH) C2R_CASE(PS, PD) C2R_CASE(PS, PS) C2R_CASE(PS, PH)
-#undef C2R_CASE
-  fail(FMV_EINVAL, "c2r: unsupported precision combination");
-}
-
-// ------------------------------------------------------------- SBGEMV ----
-struct GemvPlan {
-  GemvParams p{};
-  int block = 0;
-  size_t smem = 0;
-  int rpt = 1;
-};
-
-
-template <int MODE, class E, class O, int RPT, int V, int LPC>
-void sbgemv_launch_t(fmv_ctx* ctx, GemvPlan& gp) {
-  auto kern = k_sbgemv<MODE, E, O, RPT, V, LPC>;
-  prep_smem((const void*)kern, gp.smem);
-  static std::mutex mu;
-  static std::map<std::tuple<int, int, size_t>, int> occ_cache;
-  int occ = 0;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(ctx->device, gp.block, gp.smem);
-    auto it = occ_cache.find(key);
-    if (it == occ_cache.end()) {
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, gp.block, gp.smem));
-      occ_cache[key] = occ;
-    } else {
-      occ = it->second;
-    }
-  }
-  if (occ < 1) fail(FMV_EUNSUPPORTED, "sbgemv: staged kernel does not fit on an SM");
-  const int ctas_per_sm = std::min(occ, env_int("FMV_SBGEMV_CTAS_PER_SM", FMV_SBGEMV_MINB));
-  long P = (long)sm_count(ctx->device) * ctas_per_sm;
-  P = std::min(P, gp.p.T);
-  gp.p.P = (int)P;
-  if (MODE == GM_N) {
-    const size_t part_bytes = (size_t)(P + gp.p.batch) * gp.p.m * sizeof(typename ET<E>::A);
-    ctx->partials.ensure(part_bytes);
-    gp.p.partials = ctx->partials.p;
-    gp.p.counters = ctx->tickets((size_t)gp.p.batch);
-  }
-  launch(ctx, MODE == GM_N ? 1 : 2, [&] { launch_pdl(kern, dim3((unsigned)P), dim3(gp.block), gp.smem, ctx->stream, gp.p); });
-}
-
-template <int MODE, class E, class O>
-void sbgemv_simple_t(fmv_ctx* ctx, GemvPlan& gp) {
-  const long outs = MODE == GM_N ? gp.p.m : gp.p.n;
-  dim3 grid((unsigned)((outs + 127) / 128), (unsigned)gp.p.batch);
-  launch(ctx, MODE == GM_N ? 1 : 2, [&] { k_sbgemv_simple<MODE, E, O><<<grid, 128, 0, ctx->stream>>>(gp.p); });
-}
-
-constexpr int kConsumers = FMV_SBGEMV_CONS;  // k_sbgemv consumer threads per CTA (+1 producer warp)
-constexpr int kBlockConsumers = FMV_BLOCK_CONS;  // k_sbgemm_block consumer threads per CTA
-
-// Fills the staged-kernel plan for V-element (16-byte) row vectors; returns
-// false when the staged kernel's limits are exceeded (NoTrans: m > 4*256*V
-// rows; a stage that does not fit shared memory).
-bool plan_staged(GemvPlan& gp, int mode, size_t es, size_t accsz, int V) {
-  GemvParams& p = gp.p;
-  const long col_bytes = p.lda * (long)es;
-  const int MV0 = (p.m + V - 1) / V;
-  // short columns (one CTA per SM; tools/ab_wide.sh, tools/ab_half.sh): 3 x 48 KB,
-  // except fp64 NoTrans 4 x 32 KB (fp16 NoTrans at 4 x 32 KB drops to 5.5 TB/s:
-  // too few columns per thread per stage for its per-stage compensated fold)
-  const bool n64 = mode == GM_N && es == 16;
-  int a_target = n64 ? 32 * 1024 : 48 * 1024;
-  int nst = n64 ? 4 : 3;
-  if (mode != GM_N && MV0 > 128) {
-    // tall (Conj)Trans columns: 64-96 KB stages (>= ~6 columns), one warp per
-    // column, 3 stages when they fit the 227 KB per-CTA limit, else 2, shrunk
-    // until they fit (tools/tune_conjtrans.py)
-    const long xb = ((long)p.m * es + 32 + 127) / 128 * 128 + 128;
-    const long budget = 220 * 1024;
-    a_target = (int)std::min<long>(96 * 1024, std::max<long>(64 * 1024, 6 * col_bytes));
-    nst = 3 * ((long)a_target + 256) + 2 * xb <= budget ? 3 : 2;
-    while (a_target > col_bytes && (long)nst * (a_target + 256) + 2 * xb > budget) a_target -= (int)col_bytes;
-  }
-  a_target = env_int("FMV_SBGEMV_STAGE_BYTES", a_target);
-  int Jc = (int)std::max<long>(1, a_target / std::max<long>(col_bytes, 1));
-  const long max_a = ((long)(Jc - 1) * p.lda + p.m) * (long)es;
-  if (max_a > 96 * 1024) return false;
-  p.Jc = Jc;
-  auto up128 = [](long v) { return (int)((v + 127) / 128 * 128); };
-  p.a_slot = up128(max_a + 32);
-  const long max_x = (mode == GM_N ? (long)Jc : (long)p.m) * (long)es;
-  p.x_slot = up128(max_x + 32);
-  p.nstage = std::max(2, std::min(16, env_int("FMV_SBGEMV_STAGES", nst)));
-  size_t red = 0;
-  const int MV = (p.m + V - 1) / V;
-  if (mode == GM_N) {
-    int rpt = 1;
-    while ((MV + rpt - 1) / rpt > kConsumers) rpt *= 2;
-    if (rpt > 4) return false;
-    const int rpt_env = env_int("FMV_SBGEMV_RPT", 0);
-    if ((rpt_env == 2 || rpt_env == 4) && rpt_env > rpt) rpt = rpt_env;
-    p.RT = (MV + rpt - 1) / rpt;
-    p.G = std::max(1, kConsumers / p.RT);
-    const int ncons = (p.RT * p.G + 31) / 32 * 32;
-    gp.block = ncons + 32;
-    gp.rpt = rpt;
-    red = (size_t)p.G * p.m * accsz;
-  } else {
-    // lanes per column: about <= 8 row vectors per lane for short columns,
-    // whole warps (or several warps, combined in shared memory) for tall
-    // ones; widen when a stage holds too few columns to keep 8 warps busy.
-    // (fp16 C2 columns, 25 vectors: 4.9 TB/s with 8 lanes, 6.3 with 2, 6.5 with 4)
-    int lpc = MV <= 16 ? 2 : MV <= 32 ? 4 : MV <= 128 ? 8 : MV <= 2048 ? 32 : 64;
-    if (lpc > 32) {  // very tall columns: several warps per column
-      while (lpc < kConsumers && lpc * 8 < MV) lpc *= 2;
-      while ((long)Jc * lpc < kConsumers && lpc < kConsumers) lpc *= 2;
-    }
-    const int lpc_env = env_int("FMV_SBGEMV_LPC", 0);
-    if (lpc_env == 2 || lpc_env == 4 || lpc_env == 8 || lpc_env == 32 || lpc_env == 64 || lpc_env == 128 ||
-        lpc_env == 256)
-      lpc = lpc_env;
-    p.LPC = lpc;
-    red = (size_t)(kConsumers / 32) * accsz;
-    gp.block = kConsumers + 32;
-  }
-  // (Conj)Trans: keep x_b resident when every batch entry spans >= nstage stages
-  p.xres = 0;
-  p.xres_slot = 0;
-  p.arrive_all = env_int("FMV_SBGEMV_ARRIVE_ALL", 0);
-  if (mode != GM_N && (p.n + Jc - 1) / Jc >= p.nstage && env_int("FMV_SBGEMV_XRES", 1)) {
-    p.xres = 1;
-    p.xres_slot = p.x_slot;
-  }
-  gp.smem = 512 + (size_t)p.nstage * (p.a_slot + (p.xres ? 0 : p.x_slot)) + 2 * (size_t)p.xres_slot +
-            (red + 127) / 128 * 128;
-  if (gp.smem > 227 * 1024) return false;
-  return true;
-}
-
-template <int MODE, class E, class O, int V>
-void sbgemv_staged_v(fmv_ctx* ctx, GemvPlan& gp) {
-  if constexpr (MODE == GM_N) {
-    if (gp.rpt == 1) sbgemv_launch_t<MODE, E, O, 1, V, 0>(ctx, gp);
-    else if (gp.rpt == 2) sbgemv_launch_t<MODE, E, O, 2, V, 0>(ctx, gp);
-    else sbgemv_launch_t<MODE, E, O, 4, V, 0>(ctx, gp);
-  } else {
-    if (gp.p.LPC == 2) sbgemv_launch_t<MODE, E, O, 1, V, 2>(ctx, gp);
-    else if (gp.p.LPC == 4) sbgemv_launch_t<MODE, E, O, 1, V, 4>(ctx, gp);
-    else if (gp.p.LPC == 8) sbgemv_launch_t<MODE, E, O, 1, V, 8>(ctx, gp);
-    else if (gp.p.LPC == 32) sbgemv_launch_t<MODE, E, O, 1, V, 32>(ctx, gp);
-    else sbgemv_launch_t<MODE, E, O, 1, V, 0>(ctx, gp);  // multi-warp columns
-  }
-}
-
-template <int MODE, class E, class O>
-void sbgemv_run_t(fmv_ctx* ctx, GemvPlan& gp, bool force_simple, int* used) {
-  constexpr int VMAX = (int)(16 / sizeof(E));
-  // 16-byte row vectors need 16-byte aligned columns (and x for (Conj)Trans)
-  const auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  bool vec = VMAX > 1 && gp.p.lda % VMAX == 0 && gp.p.sa % VMAX == 0 && al16(gp.p.A);
-  if (MODE != GM_N) vec = vec && gp.p.sx % VMAX == 0 && al16(gp.p.x);
-  const int V = vec ? VMAX : 1;
-  const bool staged = !force_simple && plan_staged(gp, MODE, sizeof(E), sizeof(typename ET<E>::A), V);
-  if (used) *used = staged ? 0 : 1;
-  if (!staged) {
-    sbgemv_simple_t<MODE, E, O>(ctx, gp);
-    return;
-  }
-  if constexpr (VMAX > 1) {
-    if (vec) {
-      sbgemv_staged_v<MODE, E, O, VMAX>(ctx, gp);
-      return;
-    }
-  }
-  sbgemv_staged_v<MODE, E, O, 1>(ctx, gp);
-}
-
-template <class E, class O>
-void sbgemv_mode(fmv_ctx* ctx, int mode, GemvPlan& gp, bool force_simple, int* used) {
-  if (mode == GM_N) sbgemv_run_t<GM_N, E, O>(ctx, gp, force_simple, used);
-  else if (mode == GM_T) sbgemv_run_t<GM_T, E, O>(ctx, gp, force_simple, used);
-  else sbgemv_run_t<GM_C, E, O>(ctx, gp, force_simple, used);
-}
-
-GemvPlan make_gemv(const void* A, long m, long n, long batch, long lda, long sa, const void* x, long sx, void* y,
-                   long sy) {
-  GemvPlan gp;
-  GemvParams& p = gp.p;
-  p.A = static_cast<const unsigned char*>(A);
-  p.lda = lda;
-  p.sa = sa;
-  p.x = static_cast<const unsigned char*>(x);
-  p.sx = sx;
-  p.y = static_cast<unsigned char*>(y);
-  p.sy = sy;
-  p.m = (int)m;
-  p.n = n;
-  p.batch = batch;
-  p.T = batch * n;
-  return gp;
-}
 
 // ------------------------------------------------------------ pipeline ----
 const void* op_bins(fmv_ctx* ctx, fmv_op* op, int prec, long* lda);
-
-template <class E>
-void run_gemv_o(fmv_ctx* ctx, int p3, int mode, GemvPlan& gp) {
-  if (p3 == PD) sbgemv_mode<E, double2>(ctx, mode, gp, false, nullptr);
-  else sbgemv_mode<E, float2>(ctx, mode, gp, false, nullptr);
-}
-void run_gemv(fmv_ctx* ctx, const std::array<int, 5>& p, int mode, GemvPlan& gp) {
-  if (p[2] == PD) run_gemv_o<double2>(ctx, p[3], mode, gp);
-  else if (p[2] == PS) run_gemv_o<float2>(ctx, p[3], mode, gp);
-  else run_gemv_o<__half2>(ctx, p[3], mode, gp);
-}
 
 // Column chunking of the operator for the host-I/O pipeline (a function of
 // shape, SBGEMV precision and direction only). Chunk sizes grow (F) or shrink
@@ -1020,18 +201,28 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
   auto gemv_chunk = [&](int c) {
     const long j0 = chunk_edge(n, c, C), j1 = chunk_edge(n, c + 1, C);
     const void* A = static_cast<const unsigned char*>(bins) + j0 * lda * (long)e2;
-    GemvPlan gp;
+    GemvArgs g;
+    g.A = A;
+    g.m = m;
+    g.n = j1 - j0;
+    g.batch = nb;
+    g.lda = lda;
+    g.sa = n * lda;
     if (fwd) {
-      gp = make_gemv(A, m, j1 - j0, nb, lda, n * lda, static_cast<unsigned char*>(ctx->x.p) + j0 * e2, sx, ctx->y.p,
-                     m);
+      g.x = static_cast<unsigned char*>(ctx->x.p) + j0 * e2;
+      g.sx = sx;
+      g.y = ctx->y.p;
+      g.sy = m;
       ctx->yacc.ensure((size_t)nb * m * 16 + 256);
-      gp.p.yacc = ctx->yacc.p;
-      gp.p.accum = C == 1 ? 0 : c == 0 ? 1 : c == C - 1 ? 3 : 2;
+      g.yacc = ctx->yacc.p;
+      g.accum = C == 1 ? 0 : c == 0 ? 1 : c == C - 1 ? 3 : 2;
     } else {
-      gp = make_gemv(A, m, j1 - j0, nb, lda, n * lda, ctx->x.p, sx, static_cast<unsigned char*>(ctx->y.p) + j0 * e3,
-                     n);
+      g.x = ctx->x.p;
+      g.sx = sx;
+      g.y = static_cast<unsigned char*>(ctx->y.p) + j0 * e3;
+      g.sy = n;
     }
-    run_gemv(ctx, p, fwd ? GM_N : GM_C, gp);
+    gemv_run(ctx, p[2], p[3], fwd ? FMV_GEMV_N : FMV_GEMV_C, g);
   };
   // Phases 4-5 (+ reorder back to SOTI, 1/L in cfg[3], unpad, cast cfg[4]) over series [s0, s1).
   auto c2r_series = [&](long s0, long s1) {
@@ -1113,89 +304,6 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
   g_casts.fetch_add(count_casts(p, payload_prec >= 0), std::memory_order_relaxed);
 }
 
-// ------------------------------------------------- block (multi-RHS) ----
-// K right-hand sides through one pipeline, the per-bin
-// SBGEMV replaced by the block kernel (fmv_sbgemm_block.cuh) that streams the
-// operator once for up to kBlockMax RHS.
-// RHS per block-SBGEMV launch (measured at C2, tools/bench_block.py): F
-// gains up to 8 (3.6x per-RHS throughput at fp64), F* peaks at 4 (2.6x).
-constexpr int kBlockMax = 8;
-inline int block_max(bool fwd) { return fwd ? kBlockMax : 4; }
-
-// Stage plan for k_sbgemm_block: ~32 KB of columns per stage, shrunk until
-// two CTAs fit an SM; false if the shape is outside the kernel's limits.
-bool plan_block(GemvPlan& gp, int mode, size_t es, size_t accsz, int KR) {
-  GemvParams& p = gp.p;
-  if (p.m < 1 || (mode == GM_N && p.m > kBlockConsumers)) return false;
-  auto up128 = [](long v) { return (int)((v + 127) / 128 * 128); };
-  const long col_bytes = std::max<long>(1, p.lda * (long)es);
-  const long budget = FMV_BLOCK_MINB >= 2 ? 110 * 1024 : 220 * 1024;  // fit FMV_BLOCK_MINB CTAs per SM
-  p.nstage = 3;
-  int Jc = (int)std::max<long>(1, env_int("FMV_BLOCK_STAGE_BYTES", FMV_BLOCK_MINB >= 2 ? 32768 : 65536) / col_bytes);
-  size_t red = 0;
-  if (mode == GM_N) {
-    p.RT = p.m;
-    p.G = std::max(1, kBlockConsumers / p.RT);
-    gp.block = (p.RT * p.G + 31) / 32 * 32 + 32;
-  } else {
-    gp.block = kBlockConsumers + 32;
-  }
-  for (;;) {
-    const long max_a = ((long)(Jc - 1) * p.lda + p.m) * (long)es;
-    p.Jc = Jc;
-    p.a_slot = up128(max_a + 32);
-    p.xr_slot = up128((mode == GM_N ? (long)Jc : (long)p.m) * (long)es + 32);
-    p.xres = mode != GM_N && (p.n + Jc - 1) / Jc >= p.nstage;
-    p.xres_slot = 0;
-    red = mode == GM_N ? (size_t)p.G * KR * p.m * accsz : 0;
-    const long xs = (long)KR * p.xr_slot;
-    gp.smem = 512 + (size_t)p.nstage * (p.a_slot + (p.xres ? 0 : xs)) + (p.xres ? 2 * xs : 0) + (red + 127) / 128 * 128;
-    if ((long)gp.smem <= budget || Jc == 1) break;
-    Jc = std::max(1, Jc * 3 / 4);
-  }
-  p.arrive_all = env_int("FMV_SBGEMV_ARRIVE_ALL", 0);  // racecheck mode, as k_sbgemv
-  return gp.smem <= 227 * 1024 && (long)(p.Jc - 1) * p.lda * (long)es + p.m * (long)es <= 96 * 1024;
-}
-
-template <int MODE, class E, class O, int KR, int LPC>
-void sbgemm_block_launch_t(fmv_ctx* ctx, GemvPlan& gp) {
-  auto kern = k_sbgemm_block<MODE, E, O, KR, LPC>;
-  prep_smem((const void*)kern, gp.smem);
-  int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, gp.block, gp.smem));
-  if (occ < 1) fail(FMV_EUNSUPPORTED, "block sbgemv: kernel does not fit on an SM");
-  long P = (long)sm_count(ctx->device) * std::min(occ, FMV_BLOCK_MINB);
-  P = std::min(P, gp.p.T);
-  gp.p.P = (int)P;
-  if (MODE == GM_N) {
-    ctx->partials.ensure((size_t)(P + gp.p.batch) * KR * gp.p.m * sizeof(typename ET<E>::A));
-    gp.p.partials = ctx->partials.p;
-    gp.p.counters = ctx->tickets((size_t)gp.p.batch);
-  }
-  launch(ctx, MODE == GM_N ? 1 : 2, [&] { kern<<<(unsigned)P, gp.block, gp.smem, ctx->stream>>>(gp.p); });
-}
-
-template <int MODE, class E, class O>
-bool sbgemm_block_t(fmv_ctx* ctx, GemvPlan& gp) {
-  const int K = gp.p.K;
-  const int KR = K <= 2 ? 2 : K <= 4 ? 4 : 8;
-  if (!plan_block(gp, MODE, sizeof(E), sizeof(typename ET<E>::A), KR)) return false;
-  // ConjTrans lanes per column: 8 for columns up to 128 elements, else a warp
-  constexpr int L1 = MODE == GM_N ? 0 : 8, L2 = MODE == GM_N ? 0 : 32;
-  const bool wide = MODE != GM_N && gp.p.m > 128;
-  if (KR == 2) wide ? sbgemm_block_launch_t<MODE, E, O, 2, L2>(ctx, gp) : sbgemm_block_launch_t<MODE, E, O, 2, L1>(ctx, gp);
-  else if (KR == 4) wide ? sbgemm_block_launch_t<MODE, E, O, 4, L2>(ctx, gp) : sbgemm_block_launch_t<MODE, E, O, 4, L1>(ctx, gp);
-  else wide ? sbgemm_block_launch_t<MODE, E, O, 8, L2>(ctx, gp) : sbgemm_block_launch_t<MODE, E, O, 8, L1>(ctx, gp);
-  return true;
-}
-
-template <class E>
-bool sbgemm_block_e(fmv_ctx* ctx, int p3, int mode, GemvPlan& gp) {
-  if (mode == GM_N)
-    return p3 == PD ? sbgemm_block_t<GM_N, E, double2>(ctx, gp) : sbgemm_block_t<GM_N, E, float2>(ctx, gp);
-  return p3 == PD ? sbgemm_block_t<GM_C, E, double2>(ctx, gp) : sbgemm_block_t<GM_C, E, float2>(ctx, gp);
-}
-
 // Can the block kernel run this (op, cfg)? (fp16 'h' SBGEMV and NoTrans with
 // nd > 256 rows run as K single-RHS pipelines instead.)
 bool block_supported(const fmv_op* op, int kind, const std::array<int, 5>& p) {
@@ -1235,13 +343,21 @@ void pipeline_block(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<
   const int kmax = block_max(fwd);
   for (long r0 = 0; r0 < K; r0 += kmax) {
     const int kc = (int)std::min<long>(kmax, K - r0);
-    GemvPlan gp = make_gemv(bins, m, n, nb, lda, n * lda, static_cast<unsigned char*>(ctx->x.p) + r0 * sx * e2, K * sx,
-                            static_cast<unsigned char*>(ctx->y.p) + r0 * n_out * e3, K * n_out);
-    gp.p.K = kc;
-    gp.p.sxr = sx;
-    gp.p.syr = n_out;
-    const int mode = fwd ? GM_N : GM_C;
-    const bool ok = p[2] == PD ? sbgemm_block_e<double2>(ctx, p[3], mode, gp) : sbgemm_block_e<float2>(ctx, p[3], mode, gp);
+    GemvArgs g;
+    g.A = bins;
+    g.m = m;
+    g.n = n;
+    g.batch = nb;
+    g.lda = lda;
+    g.sa = n * lda;
+    g.x = static_cast<unsigned char*>(ctx->x.p) + r0 * sx * e2;
+    g.sx = K * sx;
+    g.y = static_cast<unsigned char*>(ctx->y.p) + r0 * n_out * e3;
+    g.sy = K * n_out;
+    g.K = kc;
+    g.sxr = sx;
+    g.syr = n_out;
+    const bool ok = block_gemv_run(ctx, p[2], p[3], fwd ? FMV_GEMV_N : FMV_GEMV_C, g);
     if (!ok) fail(FMV_EUNSUPPORTED, "block sbgemv: shape outside the staged kernel's limits");
   }
   // phases 4-5 over the K*n_out series
@@ -1279,11 +395,6 @@ __global__ void k_d2h(const double* __restrict__ in, __half* __restrict__ out, l
     out[e] = __double2half(in[e]);
 }
 
-unsigned grid_for(long n, int block, int dev) {
-  const long want = (n + block - 1) / block;
-  const long cap = (long)sm_count(dev) * 16;
-  return (unsigned)std::max<long>(1, std::min(want, cap));
-}
 
 void materialize(fmv_ctx* ctx, fmv_op* op, int prec) {
   std::lock_guard<std::mutex> lk(op->mu);
@@ -1343,7 +454,6 @@ void check_same_device(const fmv_ctx* ctx, const fmv_op* op) {
 }
 
 }  // namespace
-
 // ======================================================================
 // C ABI
 // ======================================================================
@@ -1784,69 +894,8 @@ int fmv_matvec_payload(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg
   });
 }
 
-int fmv_fft_r2c(fmv_ctx* ctx, size_t L, size_t batch, char prec, const void* d_in, void* d_out) {
-  return guarded([&] {
-    if (!ctx || !d_in || !d_out) fail(FMV_EINVAL, "fft: null argument");
-    if (L < 2 || L % 2) fail(FMV_EINVAL, "FftPlan: length must be even and >= 2");
-    if (batch < 1) fail(FMV_EINVAL, "FftPlan: batch must be >= 1");
-    DeviceGuard dg(ctx->device);
-    const long nb = (long)L / 2 + 1;
-    if (prec == 'd')
-      r2c_t<PD, PD, PD, double>(ctx, static_cast<const double*>(d_in), (long)L, 1, (long)batch, (int)L / 2, (int)L,
-                                d_out, 1, nb);
-    else if (prec == 's')
-      r2c_t<PS, PS, PS, float>(ctx, static_cast<const float*>(d_in), (long)L, 1, (long)batch, (int)L / 2, (int)L,
-                               d_out, 1, nb);
-    else
-      fail(FMV_EINVAL, "fft: prec must be 'd' or 's'");
-  });
-}
-
-int fmv_fft_c2r(fmv_ctx* ctx, size_t L, size_t batch, char prec, const void* d_in, void* d_out) {
-  return guarded([&] {
-    if (!ctx || !d_in || !d_out) fail(FMV_EINVAL, "fft: null argument");
-    if (L < 2 || L % 2) fail(FMV_EINVAL, "FftPlan: length must be even and >= 2");
-    if (batch < 1) fail(FMV_EINVAL, "FftPlan: batch must be >= 1");
-    DeviceGuard dg(ctx->device);
-    const long nb = (long)L / 2 + 1;
-    if (prec == 'd')
-      c2r_t<PD, PD, double>(ctx, d_in, 1, nb, (long)batch, (int)L / 2, (int)L, static_cast<double*>(d_out), (long)L);
-    else if (prec == 's')
-      c2r_t<PS, PS, float>(ctx, d_in, 1, nb, (long)batch, (int)L / 2, (int)L, static_cast<float*>(d_out), (long)L);
-    else
-      fail(FMV_EINVAL, "fft: prec must be 'd' or 's'");
-  });
-}
-
 uint64_t fmv_casts_performed(void) { return g_casts.load(std::memory_order_relaxed); }
 void fmv_reset_cast_counter(void) { g_casts.store(0, std::memory_order_relaxed); }
-
-int fmv_sbgemv(fmv_ctx* ctx, int mode, char dtype, size_t m, size_t n, size_t batch, size_t lda, size_t stride_a,
-               const void* A, size_t stride_x, const void* x, size_t stride_y, void* y, int force_simple,
-               int* kernel_used) {
-  return guarded([&] {
-    if (!ctx || !A || !x || !y) fail(FMV_EINVAL, "gemv: null argument");
-    if (m == 0 || n == 0 || batch == 0) fail(FMV_EINVAL, "gemv: empty matrix batch");
-    if (lda < m) fail(FMV_EINVAL, "gemv: lda < rows");
-    if (mode < 0 || mode > 2) fail(FMV_EINVAL, "gemv: bad mode");
-    DeviceGuard dg(ctx->device);
-    GemvPlan gp = make_gemv(A, (long)m, (long)n, (long)batch, (long)lda, (long)stride_a, x, (long)stride_x, y,
-                            (long)stride_y);
-    const bool fs = force_simple != 0;
-    switch (dtype) {
-      case 'z': sbgemv_mode<double2, double2>(ctx, mode, gp, fs, kernel_used); break;
-      case 'c': sbgemv_mode<float2, float2>(ctx, mode, gp, fs, kernel_used); break;
-      case 'h': sbgemv_mode<__half2, float2>(ctx, mode, gp, fs, kernel_used); break;
-      case 'd':
-        sbgemv_mode<double, double>(ctx, mode == GM_C ? GM_T : mode, gp, fs, kernel_used);
-        break;
-      case 's':
-        sbgemv_mode<float, float>(ctx, mode == GM_C ? GM_T : mode, gp, fs, kernel_used);
-        break;
-      default: fail(FMV_EINVAL, "gemv: dtype must be s/d/c/z/h");
-    }
-  });
-}
 
 int fmv_comm_unique_id(void* out128) {
   return guarded([&] {
@@ -2089,3 +1138,4 @@ int fmv_graph_destroy(fmv_graph* g) {
 }
 
 }  // extern "C"
+

@@ -1,0 +1,248 @@
+// fmv_fft_launch.cu -- dispatch of the batched real FFT kernels
+// (fmv_fft.cuh) for the pipeline (phases 1-2 and 4-5, matvec.hpp:83-205),
+// operator setup (operator.hpp:99-125) and the C ABI fmv_fft_r2c / c2r
+// (fft.hpp:110-148).
+#include "fmv_runtime.cuh"
+#include "fmv_fft.cuh"
+
+namespace fmv {
+namespace rt {
+
+// ======================================================================
+// FFT geometry of the general mixed-radix kernels
+// ======================================================================
+inline FftGeom make_geom(int Nt, int nout) {
+  FftGeom g{};
+  g.N = Nt;
+  g.L = 2 * Nt;
+  g.n_div = FastDiv((uint32_t)Nt);
+  g.nb_div = FastDiv((uint32_t)Nt + 1);
+  g.nout_div = FastDiv((uint32_t)nout);
+  int n = Nt;
+  while (n > 1) {
+    int r;
+    if (n % 8 == 0 && n != 16) r = 8;  // 16 = 4*4 beats 8*2
+    else if (n % 4 == 0) r = 4;
+    else if (n % 2 == 0) r = 2;
+    else if (n % 5 == 0) r = 5;
+    else if (n % 3 == 0) r = 3;
+    else {
+      r = 7;
+      while (n % r) r += 2;  // smallest remaining odd prime factor >= 7
+    }
+    if (g.nst >= kMaxStages) fail(FMV_EUNSUPPORTED, "FFT: too many stages");
+    g.radix[g.nst++] = r;
+    n /= r;
+  }
+  int Ns = 1;
+  for (int st = 0; st < g.nst; ++st) {
+    g.nr_div[st] = FastDiv((uint32_t)(Nt / g.radix[st]));
+    g.ns_div[st] = FastDiv((uint32_t)Ns);
+    g.span_div[st] = FastDiv((uint32_t)(Ns * g.radix[st]));
+    Ns *= g.radix[st];
+  }
+  return g;
+}
+
+int fft_lg_series_per_cta(int N, size_t celem) {
+  const size_t per = 2 * (size_t)(N + 1) * celem;
+  if (per > 200 * 1024)
+    fail(FMV_EUNSUPPORTED, "FFT: n_t = " + std::to_string(N) + " exceeds the shared-memory FFT capacity");
+  const size_t budget = (size_t)env_int("FMV_FFT_SMEM_BUDGET", 64 * 1024);
+  int lg = 0;
+  while (lg < 4 && per * ((size_t)2 << lg) <= budget) ++lg;
+  return lg;
+}
+
+// Register-resident FFT kernels (fmv_fft.cuh k_r2c_reg / k_c2r_reg) cover
+// N = 1000 (10^3) and N = 100 (10^2), SOTI <-> TOSI; everything else (and
+// FMV_FFT_LEGACY=1) uses the general mixed-radix kernels.
+#ifndef FMV_FFT_S64
+#define FMV_FFT_S64 2  // fp64 Nt = 1000 series per CTA of the register FFT kernels
+#endif
+bool fft_reg_ok(int N) {
+  return (N == 1000 || N == 100) && env_int("FMV_FFT_LEGACY", 0) == 0;
+}
+
+template <int C0, int C1, int C2, class Tin, int RX, int NP, int S>
+void r2c_reg_launch(fmv_ctx* ctx, const Tin* in, long in_ss, long nseries, int nvalid, void* out, long out_ks) {
+  using R = typename PT<C1>::real;
+  using C = typename CT<R>::c;
+  const int N = RegPlan<RX, NP>::N;
+  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, 2 * N, C1, RX));
+  bool vec = (in_ss % 2 == 0) && (nvalid % 2 == 0);
+  if constexpr (sizeof(Tin) == 8) vec = vec && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  else if constexpr (sizeof(Tin) == 4) vec = vec && (reinterpret_cast<uintptr_t>(in) & 7) == 0;
+  else vec = false;
+  const long grid = (nseries + S - 1) / S;
+  constexpr size_t smem = r2c_reg_smem<C, RX, NP, S>();
+  prep_smem((const void*)k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>, smem);
+  prep_carveout((const void*)k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>);
+  launch(ctx, 0, [&] {
+    launch_pdl(k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>, dim3((unsigned)grid), dim3(S * RegPlan<RX, NP>::NR), smem,
+               ctx->stream, in, in_ss, nseries, nvalid, vec, static_cast<typename PT<C2>::cplx*>(out), out_ks, tw);
+  });
+}
+
+template <int C0, int C1, int C2, class Tin>
+void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, int N, int nvalid, void* out,
+           long out_ks, long out_ss) {
+  using R = typename PT<C1>::real;
+  using C = typename CT<R>::c;
+  constexpr bool tin_ok = sizeof(Tin) == 8 || (sizeof(Tin) == 4 && C0 == PS) || (sizeof(Tin) == 2 && C0 == PH);
+  if constexpr (tin_ok) {
+    if (in_ts == 1 && out_ss == 1 && fft_reg_ok(N)) {
+      constexpr bool f64 = sizeof(R) == 8;
+      // (fp64: one series per CTA for small batches -- more CTAs for the 100-series transforms)
+      if (N == 1000 && f64 && nseries < 1024)
+        r2c_reg_launch<C0, C1, C2, Tin, 10, 3, 1>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
+      else if (N == 1000)
+        r2c_reg_launch<C0, C1, C2, Tin, 10, 3, f64 ? FMV_FFT_S64 : 4>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
+      else
+        r2c_reg_launch<C0, C1, C2, Tin, 10, 2, f64 ? 16 : 32>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
+      return;
+    }
+  }
+  const FftGeom g = make_geom(N, nvalid);
+  const int lgS = fft_lg_series_per_cta(g.N, sizeof(C));
+  const int S = 1 << lgS;
+  const size_t smem = 2 * (size_t)S * (g.N + 1) * sizeof(C);
+  auto kern = k_r2c<C0, C1, C2, Tin>;
+  prep_smem((const void*)kern, smem);
+  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, g.L, C1));
+  const long grid = (nseries + S - 1) / S;
+  launch(ctx, 0, [&] {
+    kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(in, in_ss, in_ts, nseries, nvalid,
+                                                     static_cast<typename PT<C2>::cplx*>(out), out_ks, out_ss, g, tw, lgS);
+  });
+}
+
+// N = L/2 (complex FFT length); nvalid = input samples per series (Nt for
+// the zero-padded matvec path, L for a plain transform).
+template <class Tin>
+void r2c_dispatch(fmv_ctx* ctx, int c0, int c1, int c2, const Tin* in, long in_ss, long in_ts, long nseries, int N,
+                  int nvalid, void* out, long out_ks, long out_ss) {
+#define R2C_CASE(A, B, C)                                                                      \
+  if (c0 == A && c1 == B && c2 == C) {                                                         \
+    r2c_t<A, B, C, Tin>(ctx, in, in_ss, in_ts, nseries, N, nvalid, out, out_ks, out_ss);       \
+    return;                                                                                    \
+  }
+  R2C_CASE(PD, PD, PD) R2C_CASE(PD, PD, PS) R2C_CASE(PD, PD, PH)
+  R2C_CASE(PD, PS, PD) R2C_CASE(PD, PS, PS) R2C_CASE(PD, PS, PH)
+  R2C_CASE(PS, PD, PD) R2C_CASE(PS, PD, PS) R2C_CASE(PS, PD, PH)
+  R2C_CASE(PS, PS, PD) R2C_CASE(PS, PS, PS) R2C_CASE(PS, PS, PH)
+  R2C_CASE(PH, PD, PD) R2C_CASE(PH, PD, PS) R2C_CASE(PH, PD, PH)
+  R2C_CASE(PH, PS, PD) R2C_CASE(PH, PS, PS) R2C_CASE(PH, PS, PH)
+#undef R2C_CASE
+  fail(FMV_EINVAL, "r2c: unsupported precision combination");
+}
+
+template <int C3, int C4, class Tout, int RX, int NP, int S>
+void c2r_reg_launch(fmv_ctx* ctx, const void* in, long in_ks, long nseries, int nout, Tout* out, long out_ss) {
+  using C = typename PT<C3>::cplx;
+  const int N = RegPlan<RX, NP>::N;
+  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, 2 * N, C3, RX));
+  const bool vec = sizeof(Tout) == 8 && (out_ss % 2 == 0) && (nout % 2 == 0) &&
+                   (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  const long grid = (nseries + S - 1) / S;
+  using Cr = typename CT<typename PT<C3>::real>::c;
+  constexpr size_t smem = c2r_reg_smem<Cr, RX, NP, S>();
+  prep_smem((const void*)k_c2r_reg<C3, C4, Tout, RX, NP, S>, smem);
+  prep_carveout((const void*)k_c2r_reg<C3, C4, Tout, RX, NP, S>);
+  launch(ctx, 3, [&] {
+    launch_pdl(k_c2r_reg<C3, C4, Tout, RX, NP, S>, dim3((unsigned)grid), dim3(S * RegPlan<RX, NP>::NR), smem,
+               ctx->stream, static_cast<const C*>(in), in_ks, nseries, nout, vec, out, out_ss, tw);
+  });
+}
+
+template <int C3, int C4, class Tout>
+void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, int N, int nout, Tout* out,
+           long out_ss) {
+  using C = typename PT<C3>::cplx;
+  if (in_ss == 1 && fft_reg_ok(N)) {
+    constexpr bool f64 = C3 == PD;
+    if (N == 1000)
+    {
+      // fp32: 8 series per CTA for the big (Nm-series) transform, 2 for the small
+      // one (tools/tune_fft.py at C2: 45.5 -> 39.3 us, and 10.5 us)
+      if constexpr (f64) {
+        if (nseries < 1024) c2r_reg_launch<C3, C4, Tout, 10, 3, 1>(ctx, in, in_ks, nseries, nout, out, out_ss);
+        else c2r_reg_launch<C3, C4, Tout, 10, 3, FMV_FFT_S64>(ctx, in, in_ks, nseries, nout, out, out_ss);
+      }
+      else if (nseries >= 1024) c2r_reg_launch<C3, C4, Tout, 10, 3, 8>(ctx, in, in_ks, nseries, nout, out, out_ss);
+      else c2r_reg_launch<C3, C4, Tout, 10, 3, 2>(ctx, in, in_ks, nseries, nout, out, out_ss);
+    }
+    else
+      c2r_reg_launch<C3, C4, Tout, 10, 2, f64 ? 16 : 32>(ctx, in, in_ks, nseries, nout, out, out_ss);
+    return;
+  }
+  const FftGeom g = make_geom(N, nout);
+  const int lgS = fft_lg_series_per_cta(g.N, sizeof(C));
+  const int S = 1 << lgS;
+  const size_t smem = 2 * (size_t)S * (g.N + 1) * sizeof(C);
+  auto kern = k_c2r<C3, C4, Tout>;
+  prep_smem((const void*)kern, smem);
+  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, g.L, C3));
+  const long grid = (nseries + S - 1) / S;
+  launch(ctx, 3, [&] {
+    kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(static_cast<const C*>(in), in_ks, in_ss, nseries, nout, out,
+                                                     out_ss, g, tw, lgS);
+  });
+}
+
+void c2r_dispatch(fmv_ctx* ctx, int c3, int c4, const void* in, long in_ks, long in_ss, long nseries, int N,
+                  int nout, double* out, long out_ss) {
+#define C2R_CASE(A, B)                                                              \
+  if (c3 == A && c4 == B) {                                                         \
+    c2r_t<A, B, double>(ctx, in, in_ks, in_ss, nseries, N, nout, out, out_ss);      \
+    return;                                                                         \
+  }
+  C2R_CASE(PD, PD) C2R_CASE(PD, PS) C2R_CASE(PD, PH) C2R_CASE(PS, PD) C2R_CASE(PS, PS) C2R_CASE(PS, PH)
+#undef C2R_CASE
+  fail(FMV_EINVAL, "c2r: unsupported precision combination");
+}
+
+template void r2c_dispatch<double>(fmv_ctx*, int, int, int, const double*, long, long, long, int, int, void*, long, long);
+template void r2c_dispatch<float>(fmv_ctx*, int, int, int, const float*, long, long, long, int, int, void*, long, long);
+template void r2c_dispatch<__half>(fmv_ctx*, int, int, int, const __half*, long, long, long, int, int, void*, long, long);
+
+}  // namespace rt
+}  // namespace fmv
+
+extern "C" {
+
+int fmv_fft_r2c(fmv_ctx* ctx, size_t L, size_t batch, char prec, const void* d_in, void* d_out) {
+  return guarded([&] {
+    if (!ctx || !d_in || !d_out) fail(FMV_EINVAL, "fft: null argument");
+    if (L < 2 || L % 2) fail(FMV_EINVAL, "FftPlan: length must be even and >= 2");
+    if (batch < 1) fail(FMV_EINVAL, "FftPlan: batch must be >= 1");
+    DeviceGuard dg(ctx->device);
+    const long nb = (long)L / 2 + 1;
+    if (prec == 'd')
+      r2c_t<PD, PD, PD, double>(ctx, static_cast<const double*>(d_in), (long)L, 1, (long)batch, (int)L / 2, (int)L,
+                                d_out, 1, nb);
+    else if (prec == 's')
+      r2c_t<PS, PS, PS, float>(ctx, static_cast<const float*>(d_in), (long)L, 1, (long)batch, (int)L / 2, (int)L,
+                               d_out, 1, nb);
+    else
+      fail(FMV_EINVAL, "fft: prec must be 'd' or 's'");
+  });
+}
+
+int fmv_fft_c2r(fmv_ctx* ctx, size_t L, size_t batch, char prec, const void* d_in, void* d_out) {
+  return guarded([&] {
+    if (!ctx || !d_in || !d_out) fail(FMV_EINVAL, "fft: null argument");
+    if (L < 2 || L % 2) fail(FMV_EINVAL, "FftPlan: length must be even and >= 2");
+    if (batch < 1) fail(FMV_EINVAL, "FftPlan: batch must be >= 1");
+    DeviceGuard dg(ctx->device);
+    const long nb = (long)L / 2 + 1;
+    if (prec == 'd')
+      c2r_t<PD, PD, double>(ctx, d_in, 1, nb, (long)batch, (int)L / 2, (int)L, static_cast<double*>(d_out), (long)L);
+    else if (prec == 's')
+      c2r_t<PS, PS, float>(ctx, d_in, 1, nb, (long)batch, (int)L / 2, (int)L, static_cast<float*>(d_out), (long)L);
+    else
+      fail(FMV_EINVAL, "fft: prec must be 'd' or 's'");
+  });
+}
+
+}  // extern "C"
