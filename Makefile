@@ -15,11 +15,11 @@ all: lib oracle cpp cli stub
 lib: $(PKG)/libfftmv_cuda.so
 
 # one object per translation unit so `make -j` compiles them in parallel
-OBJS := build/obj/fmv_capi.o build/obj/fmv_fft_launch.o build/obj/fmv_gemv_launch.o build/obj/fmv_host.o
+OBJS := $(patsubst $(PKG)/csrc/%.cu,build/obj/%.o,$(wildcard $(PKG)/csrc/*.cu)) build/obj/fmv_host.o
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/fftmv_cuda.h
 
 $(PKG)/libfftmv_cuda.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl -lcudart
+	$(NVCC) $(ARCH) -shared -Xlinker --no-undefined -o $@ $(OBJS) -ldl -lcudart
 	@cat build/obj/*.ptxas.log > build_ptxas.log
 
 build/obj/%.o: $(PKG)/csrc/%.cu $(HDRS)

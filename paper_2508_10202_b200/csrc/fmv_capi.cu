@@ -663,7 +663,7 @@ int fmv_ctx_destroy(fmv_ctx* ctx) {
     DeviceGuard dg(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (auto* b : {&ctx->x, &ctx->y, &ctx->yacc, &ctx->io_in, &ctx->io_out, &ctx->partials, &ctx->counters,
-                    &ctx->payload, &ctx->red})
+                    &ctx->payload, &ctx->red, &ctx->fft_scratch})
       b->release();
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     for (auto e : ctx->cev)

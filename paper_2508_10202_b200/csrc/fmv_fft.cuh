@@ -20,26 +20,11 @@
 #pragma once
 
 #include "fmv_common.cuh"
+#include "fmv_fft_plan.cuh"
 
 namespace fmv {
 
 constexpr int kMaxStages = 24;
-
-// Division by a runtime-invariant divisor with one multiply-high
-// (Granlund-Montgomery round-up method; valid for n < 2^31).
-struct FastDiv {
-  uint32_t d = 1, m = 0, s = 0;
-  FastDiv() = default;
-  explicit FastDiv(uint32_t div) : d(div) {
-    if (div > 1) {
-      while ((1u << s) < div) ++s;
-      m = (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << s) - div)) / div + 1);
-    }
-  }
-  __device__ __forceinline__ int div(int n) const {
-    return d == 1 ? n : (int)((__umulhi((uint32_t)n, m) + (uint32_t)n) >> s);
-  }
-};
 
 struct FftGeom {
   int N;  // complex length = L/2 = Nt

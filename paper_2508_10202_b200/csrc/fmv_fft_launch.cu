@@ -4,6 +4,7 @@
 // (fft.hpp:110-148).
 #include "fmv_runtime.cuh"
 #include "fmv_fft.cuh"
+#include "fmv_fft_rt.cuh"
 
 namespace fmv {
 namespace rt {
@@ -54,14 +55,225 @@ int fft_lg_series_per_cta(int N, size_t celem) {
   return lg;
 }
 
-// Register-resident FFT kernels (fmv_fft.cuh k_r2c_reg / k_c2r_reg) cover
-// N = 1000 (10^3) and N = 100 (10^2), SOTI <-> TOSI; everything else (and
-// FMV_FFT_LEGACY=1) uses the general mixed-radix kernels.
+// Kernel families, in dispatch order (FMV_FFT_PATH = auto | reg | rt | legacy
+// | global forces one for tests; FMV_FFT_LEGACY=1 is the old switch for
+// "legacy"):
+//  * reg    -- k_r2c_reg / k_c2r_reg, compile-time radix-10 plans for the
+//              pipeline's N = 1000 and N = 100 (SOTI <-> TOSI);
+//  * rt     -- k_r2c_rt / k_c2r_rt, runtime register plans for every N whose
+//              prime factors are <= 7, while a series fits shared memory;
+//  * legacy -- k_r2c / k_c2r, ping-pong shared-memory mixed radix with a
+//              generic prime stage (any N up to the two-buffer capacity;
+//              also the time-outer input of operator setup);
+//  * global -- k_fft_g*, HBM-scratch Stockham for any N (too long for shared
+//              memory, or large prime factors).
+enum FftPath { FP_AUTO, FP_REG, FP_RT, FP_LEGACY, FP_GLOBAL };
+inline FftPath fft_path() {  // (read per call: tests switch paths within one process)
+  if (env_int("FMV_FFT_LEGACY", 0)) return FP_LEGACY;
+  const char* v = getenv("FMV_FFT_PATH");
+  if (!v || !*v) return FP_AUTO;
+  const std::string s = v;
+  return s == "reg" ? FP_REG : s == "rt" ? FP_RT : s == "legacy" ? FP_LEGACY : s == "global" ? FP_GLOBAL : FP_AUTO;
+}
 #ifndef FMV_FFT_S64
 #define FMV_FFT_S64 2  // fp64 Nt = 1000 series per CTA of the register FFT kernels
 #endif
 bool fft_reg_ok(int N) {
-  return (N == 1000 || N == 100) && env_int("FMV_FFT_LEGACY", 0) == 0;
+  return (N == 1000 || N == 100) && (fft_path() == FP_AUTO || fft_path() == FP_REG);
+}
+
+// Legacy two-buffer capacity: S = 1 series of 2 (N + 1) complex in <= 200 KB.
+bool fft_legacy_fits(int N, size_t celem) { return 2 * (size_t)(N + 1) * celem <= 200 * 1024; }
+
+// Radices of the register / global plans: greedy largest-first from
+// {16, 10, 8, 7, 5, 4, 3, 2}; false if a prime factor > 7 remains.
+bool fft_factor(int N, std::vector<int>& radices) {
+  static const int cand[] = {16, 10, 8, 7, 5, 4, 3, 2};
+  radices.clear();
+  int n = N;
+  while (n > 1) {
+    bool found = false;
+    for (int r : cand)
+      if (n % r == 0) {
+        radices.push_back(r);
+        n /= r;
+        found = true;
+        break;
+      }
+    if (!found) return false;
+  }
+  return true;
+}
+
+// Runtime register plan for complex length N (fmv_fft_rt.cuh): N = R_0 *
+// RR^k with R_0, RR in {2, 3, 4, 5, 7, 8, 10, 16} (the fewest passes, then
+// the largest RR); `extra` = 1 for the c2r (N + 1 bins per series in shared
+// memory). False if N has no such form, needs more than 512 threads per
+// series or a series does not fit a CTA's shared memory.
+bool make_rt_plan(int N, size_t celem, int extra, RtPlan& P, std::vector<int>& radices, int& RR) {
+  static const int cand[] = {16, 10, 8, 7, 5, 4, 3, 2};
+  auto in_set = [](int r) { return r == 2 || r == 3 || r == 4 || r == 5 || r == 7 || r == 8 || r == 10 || r == 16; };
+  if (N < 2) return false;
+  int best_np = 1 << 30;
+  radices.clear();
+  for (int rr : cand) {
+    // N = n * rr^k with the largest k for which n is 1 or a first-pass radix
+    int n = N, k = 0, bn = -1, bk = 0;
+    for (;;) {
+      if (n == 1 && k >= 1) {
+        bn = 1;
+        bk = k;
+      } else if (in_set(n)) {
+        bn = n;
+        bk = k;
+      }
+      if (n % rr) break;
+      n /= rr;
+      ++k;
+    }
+    if (bn < 0) continue;
+    std::vector<int> rad;
+    if (bn > 1) rad.push_back(bn);
+    rad.insert(rad.end(), bk, rr);
+    if ((int)rad.size() < best_np) {
+      best_np = (int)rad.size();
+      radices = rad;
+      RR = rr;
+    }
+  }
+  if (radices.empty() || (int)radices.size() > kRtMaxPasses) return false;
+  P = RtPlan{};
+  P.N = N;
+  P.np = (int)radices.size();
+  // threads per series: enough that no thread owns more than floor(16 / R_p)
+  // butterflies of any pass (rt_hold in fmv_fft_plan.cuh)
+  P.TS = 1;
+  for (int r : radices) {
+    const int hold = std::max(1, kRtHold / r);
+    P.TS = std::max(P.TS, (N / r + hold - 1) / hold);
+  }
+  if (P.TS > 512) return false;
+  int Ns = 1, off = 2 * N;
+  for (int p = 0; p < P.np; ++p) {
+    const int R = radices[p];
+    P.radix[p] = R;
+    P.Ns[p] = Ns;
+    P.ns_div[p] = FastDiv((uint32_t)Ns);
+    P.tw_off[p] = p == 0 ? 0 : off;
+    if (p > 0) off += R * Ns;
+    P.bpt[p] = (N / R + P.TS - 1) / P.TS;  // <= max(1, 16 / R) by the choice of TS
+    Ns *= R;
+  }
+  P.SS = N + extra;
+  if (P.SS % 2 == 0) ++P.SS;  // odd stride (in elements): consecutive series start on shifted banks
+  const size_t per = (size_t)P.SS * celem;
+  if (per > 220 * 1024) return false;
+  const size_t budget = (size_t)env_int("FMV_FFT_SMEM_BUDGET", 64 * 1024);
+  P.S = 1;
+  while (P.S * 2 * P.TS <= 256 && (size_t)P.S * 2 * per <= budget) P.S *= 2;
+  return true;
+}
+
+template <class... A>
+void rt_r2c_any(int RR, A... a) {
+  switch (RR) {
+    case 16: rt_r2c_run<16>(a...); break;
+    case 10: rt_r2c_run<10>(a...); break;
+    case 8: rt_r2c_run<8>(a...); break;
+    case 7: rt_r2c_run<7>(a...); break;
+    case 5: rt_r2c_run<5>(a...); break;
+    case 4: rt_r2c_run<4>(a...); break;
+    case 3: rt_r2c_run<3>(a...); break;
+    default: rt_r2c_run<2>(a...); break;
+  }
+}
+template <class... A>
+void rt_c2r_any(int RR, A... a) {
+  switch (RR) {
+    case 16: rt_c2r_run<16>(a...); break;
+    case 10: rt_c2r_run<10>(a...); break;
+    case 8: rt_c2r_run<8>(a...); break;
+    case 7: rt_c2r_run<7>(a...); break;
+    case 5: rt_c2r_run<5>(a...); break;
+    case 4: rt_c2r_run<4>(a...); break;
+    case 3: rt_c2r_run<3>(a...); break;
+    default: rt_c2r_run<2>(a...); break;
+  }
+}
+
+template <class T>
+constexpr int prec_tag() {
+  return sizeof(T) == 8 ? PD : sizeof(T) == 4 ? PS : PH;
+}
+
+// HBM-scratch Stockham passes over z (nser x N complex, ping-pong with the
+// second half of the scratch); returns the buffer holding the result.
+template <class R, int D>
+typename CT<R>::c* global_passes(fmv_ctx* ctx, typename CT<R>::c* a, typename CT<R>::c* b, long nser, int N,
+                                 const typename CT<R>::c* tw, int cls) {
+  std::vector<int> rad;
+  const bool smooth = fft_factor(N, rad);
+  if (!smooth) {  // fixed radices for the smooth part, generic primes for the rest
+    rad.clear();
+    int n = N;
+    for (int r : {16, 10, 8, 7, 5, 4, 3, 2})
+      while (n % r == 0) {
+        rad.push_back(r);
+        n /= r;
+      }
+    for (int f = 11; n > 1; f += 2)
+      while (n % f == 0) {
+        rad.push_back(f);
+        n /= f;
+      }
+  }
+  int Ns = 1;
+  const unsigned grid = grid_for(nser * (long)N, 256, ctx->device);
+  for (int r : rad) {
+    launch(ctx, cls, [&] {
+      switch (r) {
+#define GP(RR) \
+  case RR: k_fft_gpass<R, D, RR><<<grid, 256, 0, ctx->stream>>>(a, b, nser, N, Ns, tw); break;
+        GP(2) GP(3) GP(4) GP(5) GP(7) GP(8) GP(10) GP(16)
+#undef GP
+        default: k_fft_gpass_generic<R, D><<<grid, 256, 0, ctx->stream>>>(a, b, nser, N, r, Ns, tw); break;
+      }
+    });
+    std::swap(a, b);
+    Ns *= r;
+  }
+  return a;
+}
+
+// Series per scratch round of the global path: <= 2 x 256 MB of scratch.
+inline long global_batch(long nseries, int N, size_t celem) {
+  return std::max<long>(1, std::min<long>(nseries, (256L << 20) / ((long)N * (long)celem)));
+}
+
+template <int C0, int C1, int C2, class Tin>
+void r2c_global(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, int N, int nvalid, void* out,
+                long out_ks, long out_ss) {
+  using R = typename PT<C1>::real;
+  using C = typename CT<R>::c;
+  using OutC = typename PT<C2>::cplx;
+  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, 2 * N, C1));
+  const long B = global_batch(nseries, N, sizeof(C));
+  ctx->fft_scratch.ensure(2 * (size_t)B * N * sizeof(C));
+  C* za = static_cast<C*>(ctx->fft_scratch.p);
+  C* zb = za + (size_t)B * N;
+  for (long s0 = 0; s0 < nseries; s0 += B) {
+    const long nb = std::min(B, nseries - s0);
+    const unsigned grid = grid_for(nb * (long)N, 256, ctx->device);
+    launch(ctx, 0, [&] {
+      k_fft_gpack<R, Tin><<<grid, 256, 0, ctx->stream>>>(in + s0 * in_ss, in_ss, in_ts, nb, N, nvalid, (int)C0, za);
+    });
+    C* z = global_passes<R, -1>(ctx, za, zb, nb, N, tw, 0);
+    const unsigned g2 = grid_for(nb * (long)(N + 1), 256, ctx->device);
+    launch(ctx, 0, [&] {
+      k_fft_gpost<R><<<g2, 256, 0, ctx->stream>>>(z, nb, N, static_cast<OutC*>(out) + s0 * out_ss, (int)C2, out_ks,
+                                                  out_ss, tw);
+    });
+  }
 }
 
 template <int C0, int C1, int C2, class Tin, int RX, int NP, int S>
@@ -102,6 +314,22 @@ void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, in
         r2c_reg_launch<C0, C1, C2, Tin, 10, 2, f64 ? 16 : 32>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
       return;
     }
+  }
+  const FftPath path = fft_path();
+  if (path == FP_AUTO || path == FP_RT) {
+    RtPlan P;
+    std::vector<int> radices;
+    int RR = 0;
+    if (in_ts == 1 && make_rt_plan(N, sizeof(C), 0, P, radices, RR)) {
+      const void* tw = twiddles().get_plan(ctx->device, 2 * N, C1, radices);
+      rt_r2c_any(RR, ctx, (int)C1, prec_tag<Tin>(), (int)C0, (int)C2, (const void*)in, in_ss, nseries, nvalid, out,
+                 out_ks, out_ss, (const RtPlan&)P, tw);
+      return;
+    }
+  }
+  if (path == FP_GLOBAL || !fft_legacy_fits(N, sizeof(C))) {
+    r2c_global<C0, C1, C2, Tin>(ctx, in, in_ss, in_ts, nseries, N, nvalid, out, out_ks, out_ss);
+    return;
   }
   const FftGeom g = make_geom(N, nvalid);
   const int lgS = fft_lg_series_per_cta(g.N, sizeof(C));
@@ -156,6 +384,31 @@ void c2r_reg_launch(fmv_ctx* ctx, const void* in, long in_ks, long nseries, int 
 }
 
 template <int C3, int C4, class Tout>
+void c2r_global(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, int N, int nout, Tout* out,
+                long out_ss) {
+  using R = typename PT<C3>::real;
+  using C = typename CT<R>::c;
+  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, 2 * N, C3));
+  const long B = global_batch(nseries, N, sizeof(C));
+  ctx->fft_scratch.ensure(2 * (size_t)B * N * sizeof(C));
+  C* za = static_cast<C*>(ctx->fft_scratch.p);
+  C* zb = za + (size_t)B * N;
+  for (long s0 = 0; s0 < nseries; s0 += B) {
+    const long nb = std::min(B, nseries - s0);
+    const unsigned grid = grid_for(nb * (long)N, 256, ctx->device);
+    launch(ctx, 3, [&] {
+      k_fft_gpre<R><<<grid, 256, 0, ctx->stream>>>(static_cast<const C*>(in) + s0 * in_ss, in_ks, in_ss, nb, N, za,
+                                                   tw);
+    });
+    C* z = global_passes<R, 1>(ctx, za, zb, nb, N, tw, 3);
+    const unsigned g2 = grid_for(nb * (long)nout, 256, ctx->device);
+    launch(ctx, 3, [&] {
+      k_fft_gunpack<R, Tout><<<g2, 256, 0, ctx->stream>>>(z, nb, N, nout, (int)C4, out + s0 * out_ss, out_ss);
+    });
+  }
+}
+
+template <int C3, int C4, class Tout>
 void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, int N, int nout, Tout* out,
            long out_ss) {
   using C = typename PT<C3>::cplx;
@@ -174,6 +427,22 @@ void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, i
     }
     else
       c2r_reg_launch<C3, C4, Tout, 10, 2, f64 ? 16 : 32>(ctx, in, in_ks, nseries, nout, out, out_ss);
+    return;
+  }
+  const FftPath path = fft_path();
+  if (path == FP_AUTO || path == FP_RT) {
+    RtPlan P;
+    std::vector<int> radices;
+    int RR = 0;
+    if (make_rt_plan(N, sizeof(C), 1, P, radices, RR)) {
+      const void* tw = twiddles().get_plan(ctx->device, 2 * N, C3, radices);
+      rt_c2r_any(RR, ctx, (int)C3, prec_tag<Tout>(), (int)C4, in, in_ks, in_ss, nseries, nout, (void*)out, out_ss,
+                 (const RtPlan&)P, tw);
+      return;
+    }
+  }
+  if (path == FP_GLOBAL || !fft_legacy_fits(N, sizeof(C))) {
+    c2r_global<C3, C4, Tout>(ctx, in, in_ks, in_ss, nseries, N, nout, out, out_ss);
     return;
   }
   const FftGeom g = make_geom(N, nout);

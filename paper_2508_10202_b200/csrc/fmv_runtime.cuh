@@ -24,6 +24,7 @@
 
 #include "../../include/fftmv_cuda.h"
 #include "fmv_common.cuh"
+#include "fmv_fft_plan.cuh"
 
 namespace fmv {
 namespace rt {
@@ -124,19 +125,28 @@ inline size_t esize(int prec) { return prec == PD ? 16 : prec == PS ? 8 : 4; }
 // ======================================================================
 struct TwiddleCache {
   std::mutex mu;
-  // (device, L, prec, RX) -> device table; RX = 0: the base table
-  // exp(-2*pi*i*m/L), m < L; RX > 1: the base table followed by one table per
-  // register-FFT pass p = 2..NP (Ns = RX^(p-1)) laid out [q*Ns + k] =
-  // base[q*k*L/(Ns*RX)], so a warp's twiddle read for fixed q is contiguous
-  // in k (k_r2c_reg / k_c2r_reg); the values are bitwise the base table's.
-  std::map<std::tuple<int, int, int, int>, void*> tabs;
+  // (device, L, prec, radices) -> device table: the base table
+  // exp(-2*pi*i*m/L), m < L (exact at multiples of pi/2; fp32 tables hold the
+  // float-rounded values), followed -- for a register FFT plan with radices
+  // R_0..R_{np-1} -- by one table per pass p >= 1 laid out [q*Ns_p + k] =
+  // base[q*k*L/(Ns_p*R_p)] (q < R_p, k < Ns_p = R_0*...*R_{p-1}), so a warp's
+  // twiddle read for fixed q is contiguous in k (k_r2c_reg / k_c2r_reg,
+  // k_r2c_rt / k_c2r_rt); the values are bitwise the base table's.
+  std::map<std::tuple<int, int, int, std::vector<int>>, void*> tabs;
   ~TwiddleCache() {}  // tables live for the process (like the reference's plan cache, fft.hpp:152-164)
+
+  // Base table only (RX = 0) or the uniform plan RX^NP of k_r2c_reg (RX > 1).
   const void* get(int dev, int L, int prec, int RX = 0) {
+    std::vector<int> radices;
+    if (RX > 1)
+      for (int n = L / 2; n > 1; n /= RX) radices.push_back(RX);
+    return get_plan(dev, L, prec, radices);
+  }
+  const void* get_plan(int dev, int L, int prec, const std::vector<int>& radices) {
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(dev, L, prec, RX);
+    const auto key = std::make_tuple(dev, L, prec, radices);
     auto it = tabs.find(key);
     if (it != tabs.end()) return it->second;
-    // exp(-2*pi*i*m/L), long double, exact at multiples of pi/2
     std::vector<double> re(L), im(L);
     const long double pi = 3.141592653589793238462643383279502884L;
     for (int m = 0; m < L; ++m) {
@@ -151,36 +161,32 @@ struct TwiddleCache {
         c = cosl(a);
         s = sinl(a);
       }
-      re[m] = (double)c;
-      im[m] = (double)s;
-      if (prec == PS) {
-        re[m] = (double)(float)c;
-        im[m] = (double)(float)s;
-      }
+      re[m] = prec == PS ? (double)(float)c : (double)c;
+      im[m] = prec == PS ? (double)(float)s : (double)s;
     }
-    if (RX > 1) {
-      const int N = L / 2;
-      for (int Ns = RX; Ns < N; Ns *= RX) {
-        for (int q = 0; q < RX; ++q)
-          for (int k = 0; k < Ns; ++k) {
-            const int m = q * k * (L / (Ns * RX));
-            re.push_back(re[m]);
-            im.push_back(im[m]);
-          }
-      }
+    long Ns = radices.empty() ? 1 : radices[0];
+    for (size_t p = 1; p < radices.size(); ++p) {
+      const int R = radices[p];
+      for (int q = 0; q < R; ++q)
+        for (long k = 0; k < Ns; ++k) {
+          const long m = (long)q * k * (L / (Ns * R));
+          re.push_back(re[m]);
+          im.push_back(im[m]);
+        }
+      Ns *= R;
     }
-    L = (int)re.size();
+    const size_t n = re.size();
     void* d = nullptr;
     if (prec == PD) {
-      std::vector<double2> h(L);
-      for (int m = 0; m < L; ++m) h[m] = make_double2(re[m], im[m]);
-      CK(cudaMalloc(&d, L * sizeof(double2)));
-      CK(cudaMemcpy(d, h.data(), L * sizeof(double2), cudaMemcpyHostToDevice));
+      std::vector<double2> h(n);
+      for (size_t m = 0; m < n; ++m) h[m] = make_double2(re[m], im[m]);
+      CK(cudaMalloc(&d, n * sizeof(double2)));
+      CK(cudaMemcpy(d, h.data(), n * sizeof(double2), cudaMemcpyHostToDevice));
     } else {
-      std::vector<float2> h(L);
-      for (int m = 0; m < L; ++m) h[m] = make_float2((float)re[m], (float)im[m]);
-      CK(cudaMalloc(&d, L * sizeof(float2)));
-      CK(cudaMemcpy(d, h.data(), L * sizeof(float2), cudaMemcpyHostToDevice));
+      std::vector<float2> h(n);
+      for (size_t m = 0; m < n; ++m) h[m] = make_float2((float)re[m], (float)im[m]);
+      CK(cudaMalloc(&d, n * sizeof(float2)));
+      CK(cudaMemcpy(d, h.data(), n * sizeof(float2), cudaMemcpyHostToDevice));
     }
     tabs[key] = d;
     return d;
@@ -282,7 +288,7 @@ struct fmv_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  DevBuf x, y, yacc, io_in, io_out, partials, counters, payload, red;
+  DevBuf x, y, yacc, io_in, io_out, partials, counters, payload, red, fft_scratch;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t cev[34] = {};
   size_t counters_len = 0;
@@ -466,6 +472,17 @@ void r2c_dispatch(fmv_ctx* ctx, int c0, int c1, int c2, const Tin* in, long in_s
                   int nvalid, void* out, long out_ks, long out_ss);
 void c2r_dispatch(fmv_ctx* ctx, int c3, int c4, const void* in, long in_ks, long in_ss, long nseries, int N,
                   int nout, double* out, long out_ss);
+
+// Runtime-plan register FFTs (fmv_fft_rt.cuh), one explicit instantiation per
+// pass radix RR in fmv_fft_rt_{a,b,c}.cu: cr = arithmetic precision (PD/PS),
+// tin / tout = precision of the real input / output array, c0 / c2 / c4 the
+// pipeline roundings; tw = the plan's twiddle table (TwiddleCache::get_plan).
+template <int RR>
+void rt_r2c_run(fmv_ctx* ctx, int cr, int tin, int c0, int c2, const void* in, long in_ss, long nseries, int nvalid,
+                void* out, long out_ks, long out_ss, const RtPlan& P, const void* tw);
+template <int RR>
+void rt_c2r_run(fmv_ctx* ctx, int cr, int tout, int c4, const void* in, long in_ks, long in_ss, long nseries,
+                int nout, void* out, long out_ss, const RtPlan& P, const void* tw);
 
 // SBGEMV dispatch (fmv_gemv_launch.cu): y_b = op(A_b) x_b for b < batch,
 // strides in elements of the SBGEMV precision p2, output in p3.
