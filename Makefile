@@ -15,18 +15,18 @@ all: lib oracle cpp cli stub
 lib: $(PKG)/libfftmv_cuda.so
 
 # one object per translation unit so `make -j` compiles them in parallel
-OBJS := $(patsubst $(PKG)/csrc/%.cu,build/obj/%.o,$(wildcard $(PKG)/csrc/*.cu)) build/obj/fmv_host.o
+OBJS := $(patsubst $(PKG)/csrc/%.cu,build/obj/%.o,$(wildcard $(PKG)/csrc/*.cu)) $(patsubst $(PKG)/csrc/%.cpp,build/obj/%.o,$(wildcard $(PKG)/csrc/*.cpp))
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/fftmv_cuda.h
 
 $(PKG)/libfftmv_cuda.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared -Xlinker --no-undefined -o $@ $(OBJS) -ldl -lcudart
+	$(NVCC) $(ARCH) -shared -Xlinker --no-undefined -o $@ $(OBJS) -ldl -lcudart -lpthread
 	@cat build/obj/*.ptxas.log > build_ptxas.log
 
 build/obj/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p build/obj
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/obj/$*.ptxas.log || (cat build/obj/$*.ptxas.log; false)
 
-build/obj/fmv_host.o: $(PKG)/csrc/fmv_host.cpp include/fftmv_cuda.h
+build/obj/%.o: $(PKG)/csrc/%.cpp include/fftmv_cuda.h
 	@mkdir -p build/obj
 	g++ -std=c++20 -O2 -fPIC -Wall -c -o $@ $<
 

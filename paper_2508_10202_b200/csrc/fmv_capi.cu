@@ -129,10 +129,50 @@ struct StreamSwap {
   ~StreamSwap() { ctx->stream = saved; }
 };
 
+// Host side of a blocking matvec with host buffers. Pinned caller buffers are
+// copied by DMA directly; pageable ones (the reference API's std::vectors)
+// go through the context's pinned staging buffers, filled / drained by the
+// host thread pool while the GPU works on neighbouring chunks.
 struct HostIO {
   const void* h_in = nullptr;  // copy in (overlapped) to the device `in` buffer
   double* h_out = nullptr;     // copy out (overlapped) from the device `out` buffer
   size_t in_elem = 8;          // bytes per input element (a cfg[0] payload may be float / half)
+  unsigned char* pin_in = nullptr;  // staging (set when h_in is pageable)
+  double* pin_out = nullptr;        // staging (set when h_out is pageable)
+  struct Pending {
+    size_t off, count;
+    cudaEvent_t ev;
+  };
+  std::vector<Pending> pending;  // staged output chunks not yet copied to h_out
+
+  // host bytes [off, off + bytes) of the input -> device dst
+  void h2d(fmv_ctx* ctx, void* dst, size_t off, size_t bytes, cudaStream_t s) const {
+    const unsigned char* src = static_cast<const unsigned char*>(h_in) + off;
+    if (pin_in) {
+      parallel_memcpy(pin_in + off, src, bytes);
+      src = pin_in + off;
+    }
+    copy_async(ctx, 0, dst, src, bytes, cudaMemcpyHostToDevice, s);
+  }
+  // device src -> output doubles [off, off + count); staged chunks complete in drain()
+  void d2h(fmv_ctx* ctx, size_t off, const double* src, size_t count, cudaStream_t s, cudaEvent_t ev) {
+    if (!pin_out) {
+      copy_async(ctx, 4, h_out + off, src, count * sizeof(double), cudaMemcpyDeviceToHost, s);
+      return;
+    }
+    copy_async(ctx, 4, pin_out + off, src, count * sizeof(double), cudaMemcpyDeviceToHost, s);
+    CK(cudaEventRecord(ev, s));
+    pending.push_back({off, count, ev});
+  }
+  // Copy staged output chunks to h_out, all but the newest `keep`.
+  void drain(size_t keep = 0) {
+    while (pending.size() > keep) {
+      const Pending q = pending.front();
+      pending.erase(pending.begin());
+      CK(cudaEventSynchronize(q.ev));
+      parallel_memcpy(h_out + q.off, pin_out + q.off, q.count * sizeof(double));
+    }
+  }
 };
 
 cudaStream_t copy_stream(fmv_ctx* ctx) {
@@ -150,7 +190,7 @@ cudaEvent_t chunk_event(fmv_ctx* ctx, int i) {
 // host input is copied into `in` chunk by chunk (F) and the output leaves
 // chunk by chunk (F*) on a copy stream, overlapped with the SBGEMV.
 void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5>& p, const void* in,
-              int payload_prec, double* out, const HostIO* hio = nullptr) {
+              int payload_prec, double* out, HostIO* hio = nullptr) {
   fmv_op* op = const_cast<fmv_op*>(cop);
   const bool fwd = kind == FMV_FORWARD;
   const long nt = (long)op->nt, nb = (long)op->nb();
@@ -241,9 +281,8 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
       auto issue_in = [&](int c) {
         const long j0 = chunk_edge(n, c, C), j1 = chunk_edge(n, c + 1, C);
         const size_t ie = hio->in_elem;
-        copy_async(ctx, 0, const_cast<unsigned char*>(static_cast<const unsigned char*>(in)) + j0 * nt * ie,
-                   static_cast<const unsigned char*>(hio->h_in) + j0 * nt * ie, (size_t)(j1 - j0) * nt * ie,
-                   cudaMemcpyHostToDevice, ks);
+        hio->h2d(ctx, const_cast<unsigned char*>(static_cast<const unsigned char*>(in)) + j0 * nt * ie, j0 * nt * ie,
+                 (size_t)(j1 - j0) * nt * ie, ks);
         if (ovl) {
           StreamSwap sw(ctx, ks);
           r2c_series(j0, j1);
@@ -265,11 +304,10 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
       for (int c = 0; c < C; ++c) gemv_chunk(c);
     }
     c2r_series(0, n_out);
-    if (h_out) copy_async(ctx, 4, hio->h_out, out, (size_t)n_out * nt * sizeof(double), cudaMemcpyDeviceToHost, cs);
+    if (h_out) hio->d2h(ctx, 0, out, (size_t)n_out * nt, cs, chunk_event(ctx, 16));
   } else {
     if (h_in)
-      copy_async(ctx, 0, const_cast<void*>(in), hio->h_in, (size_t)n_in * nt * hio->in_elem, cudaMemcpyHostToDevice,
-                 cs);
+      hio->h2d(ctx, const_cast<void*>(in), 0, (size_t)n_in * nt * hio->in_elem, cs);
     r2c_series(0, n_in);
     if (h_out) {
       cudaStream_t ks = copy_stream(ctx);
@@ -283,8 +321,8 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
       auto issue_out = [&](int c) {
         const long j0 = chunk_edge(n, c, C), j1 = chunk_edge(n, c + 1, C);
         CK(cudaStreamWaitEvent(ks, chunk_event(ctx, c), 0));
-        copy_async(ctx, 4, hio->h_out + j0 * nt, out + j0 * nt, (size_t)(j1 - j0) * nt * sizeof(double),
-                   cudaMemcpyDeviceToHost, ks);
+        hio->d2h(ctx, j0 * nt, out + j0 * nt, (size_t)(j1 - j0) * nt, ks, chunk_event(ctx, 16 + c));
+        hio->drain(1);  // the previous staged chunk's host copy overlaps this chunk's SBGEMV
       };
       for (int c = 0; c < C; ++c) {
         const long j0 = chunk_edge(n, c, C), j1 = chunk_edge(n, c + 1, C);
@@ -620,7 +658,20 @@ void matvec_blocking(fmv_ctx* ctx, const fmv_op* op, int kind, const std::array<
     hio.h_in = in;
     hio.h_out = out;
     hio.in_elem = in_elem;
+    if (is_pageable(in)) {
+      ctx->pin_in.ensure(n_in * in_elem);
+      hio.pin_in = static_cast<unsigned char*>(ctx->pin_in.p);
+    }
+    if (is_pageable(out)) {
+      ctx->pin_out.ensure(n_out * sizeof(double));
+      hio.pin_out = static_cast<double*>(ctx->pin_out.p);
+    }
     pipeline(ctx, op, kind, p, ctx->io_in.p, payload_prec, static_cast<double*>(ctx->io_out.p), &hio);
+    if (times) CK(cudaEventRecord(ctx->te[1], s));
+    hio.drain();
+    CK(cudaStreamSynchronize(s));
+    if (times) collect_phase_times(ctx, ctx->te[0], ctx->te[1], times);
+    return;
   }
   if (times) CK(cudaEventRecord(ctx->te[1], s));
   CK(cudaStreamSynchronize(s));
@@ -665,6 +716,8 @@ int fmv_ctx_destroy(fmv_ctx* ctx) {
     for (auto* b : {&ctx->x, &ctx->y, &ctx->yacc, &ctx->io_in, &ctx->io_out, &ctx->partials, &ctx->counters,
                     &ctx->payload, &ctx->red, &ctx->fft_scratch})
       b->release();
+    ctx->pin_in.release();
+    ctx->pin_out.release();
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     for (auto e : ctx->cev)
       if (e) cudaEventDestroy(e);
@@ -995,7 +1048,7 @@ int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* op, int kind, const char*
       din = static_cast<const double*>(ctx->io_in.p);
       dout = static_cast<double*>(ctx->io_out.p);
     }
-    const HostIO* hp = io_on_device ? nullptr : &hio;
+    HostIO* hp = io_on_device ? nullptr : &hio;
     if (fwd) {
       // partition.hpp:157-182: full-length partial d per rank, summed in cfg[4].
       pipeline(ctx, op, kind, p, din, -1, dout, hp);

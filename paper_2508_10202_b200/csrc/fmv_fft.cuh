@@ -208,12 +208,16 @@ __device__ __forceinline__ void stage_fixed(const typename CT<R>::c* __restrict_
   }
 }
 
-// Any radix r (used for primes other than 2,3,5): one thread per output.
+// Any radix r (used for primes other than 2,3,5): one thread per output,
+// an O(r) DFT accumulated in fp64 with the fp64 twiddle table `twd` whatever
+// the working precision R, then rounded to R once. (A long fp32 sum over a
+// large prime -- n_t = 1009 -- would otherwise lose ~sqrt(r) ulps against the
+// reference's FFTW-style single-precision transform.)
 template <class R, int D>
 __device__ __forceinline__ void stage_generic(const typename CT<R>::c* __restrict__ src,
                                               typename CT<R>::c* __restrict__ dst, int ss, int ns, int r, int Ns,
                                               const FastDiv& nd, const FastDiv& nsd, const FastDiv& spand,
-                                              const typename CT<R>::c* __restrict__ tw, int N, int L) {
+                                              const double2* __restrict__ twd, int N, int L) {
   using C = typename CT<R>::c;
   const int Nr = N / r;
   const int span = Ns * r;
@@ -228,21 +232,22 @@ __device__ __forceinline__ void stage_generic(const typename CT<R>::c* __restric
     const int j = blk * Ns + k;
     const int estep = k + q * Ns;
     const C* in = src + s * ss;
-    C acc = {R(0), R(0)};
+    double2 acc = {0.0, 0.0};
     int e = 0;
     for (int m = 0; m < r; ++m) {
-      acc = cadd(acc, cmul(in[j + m * Nr], twiddle<D>(tw, e * tstep)));
+      const double2 x = to_cd(in[j + m * Nr]);
+      acc = cadd(acc, cmul(x, twiddle<D>(twd, e * tstep)));
       e += estep;
       if (e >= span) e -= span * (e / span);
     }
-    dst[s * ss + o] = acc;
+    dst[s * ss + o] = C{(R)acc.x, (R)acc.y};
   }
 }
 
 // Runs all stages; returns the buffer holding the result.
 template <class R, int D>
 __device__ typename CT<R>::c* run_stages(typename CT<R>::c* a, typename CT<R>::c* b, int ss, int ns, const FftGeom& g,
-                                         const typename CT<R>::c* __restrict__ tw) {
+                                         const typename CT<R>::c* __restrict__ tw, const double2* __restrict__ twd) {
   int Ns = 1;
   for (int st = 0; st < g.nst; ++st) {
     const int r = g.radix[st];
@@ -253,7 +258,7 @@ __device__ typename CT<R>::c* run_stages(typename CT<R>::c* a, typename CT<R>::c
       case 5: stage_fixed<R, D, 5>(a, b, ss, ns, Ns, g.nr_div[st], g.ns_div[st], tw, g.N, g.L); break;
       case 8: stage_fixed<R, D, 8>(a, b, ss, ns, Ns, g.nr_div[st], g.ns_div[st], tw, g.N, g.L); break;
       default:
-        stage_generic<R, D>(a, b, ss, ns, r, Ns, g.n_div, g.ns_div[st], g.span_div[st], tw, g.N, g.L);
+        stage_generic<R, D>(a, b, ss, ns, r, Ns, g.n_div, g.ns_div[st], g.span_div[st], twd, g.N, g.L);
         break;
     }
     __syncthreads();
@@ -275,7 +280,7 @@ template <int C0, int C1, int C2, class Tin>
 __global__ void __launch_bounds__(256) k_r2c(const Tin* __restrict__ in, long in_ss, long in_ts, long nseries, int nvalid,
                                              typename PT<C2>::cplx* __restrict__ out, long out_ks, long out_ss,
                                              FftGeom g, const typename CT<typename PT<C1>::real>::c* __restrict__ tw,
-                                             int lgS) {
+                                             const double2* __restrict__ twd, int lgS) {
   using R = typename PT<C1>::real;
   using C = typename CT<R>::c;
   using OutC = typename PT<C2>::cplx;
@@ -355,7 +360,7 @@ __global__ void __launch_bounds__(256) k_r2c(const Tin* __restrict__ in, long in
     }
   }
   __syncthreads();
-  const C* Z = run_stages<R, -1>(bufA, bufB, ss, ns, g, tw);
+  const C* Z = run_stages<R, -1>(bufA, bufB, ss, ns, g, tw, twd);
 
   // Real-signal post-pass: X[k] = E[k] + w^k * (-i) * D[k], k = 0..N.
   const R half = R(0.5);
@@ -388,7 +393,8 @@ __global__ void __launch_bounds__(256) k_r2c(const Tin* __restrict__ in, long in
 template <int C3, int C4, class Tout>
 __global__ void __launch_bounds__(256) k_c2r(const typename PT<C3>::cplx* __restrict__ in, long in_ks, long in_ss,
                                              long nseries, int nout, Tout* __restrict__ out, long out_ss, FftGeom g,
-                                             const typename PT<C3>::cplx* __restrict__ tw, int lgS) {
+                                             const typename PT<C3>::cplx* __restrict__ tw,
+                                             const double2* __restrict__ twd, int lgS) {
   using R = typename PT<C3>::real;
   using C = typename CT<R>::c;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -450,7 +456,7 @@ __global__ void __launch_bounds__(256) k_c2r(const typename PT<C3>::cplx* __rest
     bufB[s * ss + k] = Z;
   }
   __syncthreads();
-  const C* z = run_stages<R, 1>(bufB, bufA, ss, ns, g, tw);
+  const C* z = run_stages<R, 1>(bufB, bufA, ss, ns, g, tw, twd);
   for (int e = threadIdx.x; e < ns * nout; e += blockDim.x) {
     const int s = g.nout_div.div(e), t = e - s * nout;
     const C v = z[s * ss + (t >> 1)];

@@ -211,6 +211,7 @@ constexpr int prec_tag() {
 template <class R, int D>
 typename CT<R>::c* global_passes(fmv_ctx* ctx, typename CT<R>::c* a, typename CT<R>::c* b, long nser, int N,
                                  const typename CT<R>::c* tw, int cls) {
+  const double2* twd = static_cast<const double2*>(twiddles().get(ctx->device, 2 * N, PD));
   std::vector<int> rad;
   const bool smooth = fft_factor(N, rad);
   if (!smooth) {  // fixed radices for the smooth part, generic primes for the rest
@@ -236,7 +237,7 @@ typename CT<R>::c* global_passes(fmv_ctx* ctx, typename CT<R>::c* a, typename CT
   case RR: k_fft_gpass<R, D, RR><<<grid, 256, 0, ctx->stream>>>(a, b, nser, N, Ns, tw); break;
         GP(2) GP(3) GP(4) GP(5) GP(7) GP(8) GP(10) GP(16)
 #undef GP
-        default: k_fft_gpass_generic<R, D><<<grid, 256, 0, ctx->stream>>>(a, b, nser, N, r, Ns, tw); break;
+        default: k_fft_gpass_generic<R, D><<<grid, 256, 0, ctx->stream>>>(a, b, nser, N, r, Ns, twd); break;
       }
     });
     std::swap(a, b);
@@ -338,10 +339,12 @@ void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, in
   auto kern = k_r2c<C0, C1, C2, Tin>;
   prep_smem((const void*)kern, smem);
   const C* tw = static_cast<const C*>(twiddles().get(ctx->device, g.L, C1));
+  const double2* twd = static_cast<const double2*>(twiddles().get(ctx->device, g.L, PD));
   const long grid = (nseries + S - 1) / S;
   launch(ctx, 0, [&] {
     kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(in, in_ss, in_ts, nseries, nvalid,
-                                                     static_cast<typename PT<C2>::cplx*>(out), out_ks, out_ss, g, tw, lgS);
+                                                     static_cast<typename PT<C2>::cplx*>(out), out_ks, out_ss, g, tw,
+                                                     twd, lgS);
   });
 }
 
@@ -452,10 +455,11 @@ void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, i
   auto kern = k_c2r<C3, C4, Tout>;
   prep_smem((const void*)kern, smem);
   const C* tw = static_cast<const C*>(twiddles().get(ctx->device, g.L, C3));
+  const double2* twd = static_cast<const double2*>(twiddles().get(ctx->device, g.L, PD));
   const long grid = (nseries + S - 1) / S;
   launch(ctx, 3, [&] {
     kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(static_cast<const C*>(in), in_ks, in_ss, nseries, nout, out,
-                                                     out_ss, g, tw, lgS);
+                                                     out_ss, g, tw, twd, lgS);
   });
 }
 

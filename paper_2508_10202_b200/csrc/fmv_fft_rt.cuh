@@ -446,9 +446,10 @@ __global__ void k_fft_gpass(const typename CT<R>::c* __restrict__ src, typename 
   }
 }
 
+// (fp64 accumulation and twiddles for any working precision, as stage_generic)
 template <class R, int D>
 __global__ void k_fft_gpass_generic(const typename CT<R>::c* __restrict__ src, typename CT<R>::c* __restrict__ dst,
-                                    long nser, int N, int r, int Ns, const typename CT<R>::c* __restrict__ tw) {
+                                    long nser, int N, int r, int Ns, const double2* __restrict__ twd) {
   using C = typename CT<R>::c;
   const int NB = N / r, span = Ns * r, L = 2 * N, tstep = L / span;
   const long total = nser * (long)N;
@@ -459,10 +460,10 @@ __global__ void k_fft_gpass_generic(const typename CT<R>::c* __restrict__ src, t
     const int j = blk * Ns + k;
     const long estep = k + (long)q * Ns;
     const C* in = src + s * N;
-    C acc = {R(0), R(0)};
+    double2 acc = {0.0, 0.0};
     for (int m = 0; m < r; ++m)
-      acc = cadd(acc, cmul(in[j + m * NB], twiddle<D>(tw, (int)(((long)m * estep % span) * tstep))));
-    dst[s * N + o] = acc;
+      acc = cadd(acc, cmul(to_cd(in[j + m * NB]), twiddle<D>(twd, (int)(((long)m * estep % span) * tstep))));
+    dst[s * N + o] = C{(R)acc.x, (R)acc.y};
   }
 }
 

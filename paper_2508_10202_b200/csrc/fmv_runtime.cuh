@@ -279,6 +279,25 @@ struct DevBuf {
   }
 };
 
+// Pinned (page-locked) host buffer, grow-only: staging for pageable caller I/O.
+struct PinBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= n) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    CK(cudaHostAlloc(&p, bytes, cudaHostAllocDefault));
+    n = bytes;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
 struct ProfRec {
   int cls;
   cudaEvent_t a, b;
@@ -289,6 +308,7 @@ struct fmv_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   DevBuf x, y, yacc, io_in, io_out, partials, counters, payload, red, fft_scratch;
+  PinBuf pin_in, pin_out;  // staging for pageable host I/O (HostIO)
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t cev[34] = {};
   size_t counters_len = 0;
@@ -460,6 +480,19 @@ inline unsigned grid_for(long n, int block, int dev) {
   const long want = (n + block - 1) / block;
   const long cap = (long)sm_count(dev) * 16;
   return (unsigned)std::max<long>(1, std::min(want, cap));
+}
+
+// Host memcpy split across a small persistent thread pool (fmv_hostpool.cpp).
+void parallel_memcpy(void* dst, const void* src, size_t bytes);
+
+// Is p ordinary pageable host memory (not pinned / registered, not device)?
+inline bool is_pageable(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
 }
 
 // ---- entry points shared across the translation units ----
