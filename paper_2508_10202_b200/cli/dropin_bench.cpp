@@ -46,10 +46,31 @@ int main(int argc, char** argv) {
     for (int i = 0; i < steps; ++i) step();
     const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     const double bytes = 8.0 * (double)(nm * nt + nd * nt);
+    // breakdown: a fresh n_m*n_t output vector (what run_pipeline allocates for
+    // F*), and the raw C-ABI calls on reused pageable vectors
+    auto wall = [](auto&& fn, int reps) {
+      const auto a = std::chrono::steady_clock::now();
+      for (int i = 0; i < reps; ++i) fn();
+      return 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count() / reps;
+    };
+    const double ms_alloc = wall([&] {
+      std::vector<double> v(nm * nt);
+      sink += v[nm * nt / 2];
+    }, steps);
+    std::vector<double> dout(nd * nt), mout(nm * nt);
+    fmv_ctx* ctx = detail::thread_ctx(0);
+    const std::string c = cfg.render();
+    const double ms_f = wall([&] {
+      detail::check(fmv_matvec(ctx, op.handle(), FMV_FORWARD, c.c_str(), m.f64.data(), dout.data(), 0, nullptr));
+    }, steps);
+    const double ms_a = wall([&] {
+      detail::check(fmv_matvec(ctx, op.handle(), FMV_ADJOINT, c.c_str(), d.f64.data(), mout.data(), 0, nullptr));
+    }, steps);
     std::printf(
         "{\"ms_per_step\": %.6f, \"matvecs_per_s\": %.3f, \"steps\": %d, \"h2d_bytes_per_step\": %.0f, "
-        "\"d2h_bytes_per_step\": %.0f, \"checksum\": %.17g}\n",
-        1e3 * s / steps, 2.0 * steps / s, steps, bytes, bytes, sink);
+        "\"d2h_bytes_per_step\": %.0f, \"ms_alloc_out_vector\": %.4f, \"ms_capi_F_pageable\": %.4f, "
+        "\"ms_capi_Fstar_pageable\": %.4f, \"checksum\": %.17g}\n",
+        1e3 * s / steps, 2.0 * steps / s, steps, bytes, bytes, ms_alloc, ms_f, ms_a, sink);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "dropin_bench: %s\n", e.what());
     return 1;
