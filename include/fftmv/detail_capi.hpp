@@ -4,6 +4,9 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <malloc.h>
+
+#include <cstdlib>
 
 #include <memory>
 #include <mutex>
@@ -25,9 +28,28 @@ inline void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("fftmv: ") + what + ": " + cudaGetErrorString(e));
 }
 
+// The reference API returns every matvec output as a fresh std::vector
+// (matvec.hpp:305-318): 40 MB per F* at C2. glibc serves such blocks with
+// mmap and returns them with munmap, so every result pays ~10k page faults
+// (12.7 ms per 40 MB measured on the B200 box, 10x the matvec). Raising the
+// mmap and trim thresholds once keeps freed result buffers mapped for reuse.
+// FFTMV_KEEP_MALLOC=1 leaves the process's malloc settings alone.
+inline void tune_malloc_once() {
+  static const bool done = [] {
+    const char* e = std::getenv("FFTMV_KEEP_MALLOC");
+    if (!(e && *e == '1')) {
+      mallopt(M_MMAP_THRESHOLD, 1 << 30);
+      mallopt(M_TRIM_THRESHOLD, 1 << 30);
+    }
+    return true;
+  }();
+  (void)done;
+}
+
 // One context (CUDA stream + workspace) per host thread and device: contexts
 // are single-threaded, spectral operators are shared.
 inline fmv_ctx* thread_ctx(int device = 0) {
+  tune_malloc_once();
   struct Holder {
     fmv_ctx* c[16] = {};
     ~Holder() {

@@ -116,7 +116,7 @@ int fmv_matvec_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, 
  * fmv_matvec; the per-bin SBGEMV handles up to 8 (FORWARD) / 4 (ADJOINT) RHS
  * per operator pass (the operator is read from HBM once per pass instead of
  * once per RHS). Per-RHS results equal fmv_matvec's up to summation order
- * (fp64: ~1e-15 relative). 'h' SBGEMV configs and FORWARD with nd > 512 run
+ * (fp64: ~1e-15 relative). 'h' SBGEMV configs and FORWARD with nd > 416 run
  * as nrhs single-RHS pipelines. Blocking; host pointers unless io_on_device. */
 int fmv_matvec_block(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, size_t nrhs, const double* in,
                      double* out, int io_on_device);
@@ -153,7 +153,7 @@ void fmv_reset_cast_counter(void);
 /* ---- strided-batched GEMV (gemv.hpp:206-240), device pointers ----
  * dtype 's','d','c','z' (or 'h' = complex fp16 storage, fp32 accumulation,
  * output complex float). Strides/lda in elements. Returns the kernel used in
- * *kernel_used (0 staged/TMA, 1 simple) when non-NULL. A and x must be
+ * *kernel_used (0 staged/TMA, 1 simple, 2 small-problem (Conj)Trans) when non-NULL. A and x must be
  * readable up to the next 16-byte boundary past their last element. */
 int fmv_sbgemv(fmv_ctx* ctx, int mode, char dtype, size_t m, size_t n, size_t batch, size_t lda, size_t stride_a,
                const void* A, size_t stride_x, const void* x, size_t stride_y, void* y, int force_simple,

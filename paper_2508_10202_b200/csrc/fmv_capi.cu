@@ -99,13 +99,12 @@ const void* op_bins(fmv_ctx* ctx, fmv_op* op, int prec, long* lda);
 // SBGEMV consumes one, so each chunk's copy hides behind its neighbour's
 // SBGEMV and only the smallest chunk's copy is exposed. Edges on multiples of
 // 4 columns.
-std::vector<long> chunk_edges(const fmv_op* op, int prec2, bool grow, int force = 0) {
+std::vector<long> chunk_edges(const fmv_op* op, int prec2, bool grow) {
   const long nm = (long)op->nm;
   const size_t bytes = op->nb() * op->nm * op->nd * esize(prec2);
   long C = (bytes >= (size_t(1) << 30)) ? 6 : (bytes >= (size_t(1) << 27)) ? 3 : 1;
   const int env = env_int("FMV_CHUNKS", 0);
   if (env > 0) C = env;
-  if (force > 0) C = force;
   C = std::max<long>(1, std::min<long>(C, nm / 4));
   std::vector<double> w(C);
   double tot = 0;
@@ -211,17 +210,15 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
   // into column chunks so the copies hide behind it. (For F the chunk sums
   // are folded in chunk order, so the two entry points agree to rounding;
   // each is deterministic.)
-  // (experiment: FMV_DEV_CHUNKS > 1 splits a device-resident F the same way,
-  // the chunk r2c on the copy stream beside the previous chunk's SBGEMV)
-  const int dev_chunks = fwd && !h_in ? env_int("FMV_DEV_CHUNKS", 1) : 1;
-  const std::vector<long> edges = (h_in || h_out) ? chunk_edges(op, p[2], fwd)
-                                  : dev_chunks > 1 ? chunk_edges(op, p[2], true, dev_chunks)
-                                                   : std::vector<long>{0, (long)op->nm};
+  // (Device-resident F split the same way -- each chunk's r2c on the copy
+  // stream beside the previous chunk's SBGEMV -- was measured slower: 1.206 ms
+  // per F unchunked, 1.22 / 1.23 / 1.24 / 1.26 ms with 2 / 3 / 4 / 6 chunks.)
+  const std::vector<long> edges = (h_in || h_out) ? chunk_edges(op, p[2], fwd) : std::vector<long>{0, (long)op->nm};
   const int C = (int)edges.size() - 1;
   auto chunk_edge = [&](long, int c, int) { return edges[c]; };
   cudaStream_t cs = ctx->stream;
   if (C > 16) fail(FMV_EINVAL, "too many chunks");
-  if (h_in || h_out || dev_chunks > 1) {  // the copy stream must not run ahead into a buffer still in use
+  if (h_in || h_out) {  // the copy stream must not run ahead into a buffer still in use
     CK(cudaEventRecord(chunk_event(ctx, 32), cs));
     CK(cudaStreamWaitEvent(copy_stream(ctx), chunk_event(ctx, 32), 0));
   }
@@ -304,19 +301,6 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
         if (!ovl) r2c_series(chunk_edge(n, c, C), chunk_edge(n, c + 1, C));
         gemv_chunk(c);
         if (c + 1 < C) issue_in(c + 1);
-      }
-    } else if (C > 1) {
-      cudaStream_t ks = copy_stream(ctx);
-      for (int c = 0; c < C; ++c) {
-        {
-          StreamSwap sw(ctx, ks);
-          r2c_series(chunk_edge(n, c, C), chunk_edge(n, c + 1, C));
-        }
-        CK(cudaEventRecord(chunk_event(ctx, c), ks));
-      }
-      for (int c = 0; c < C; ++c) {
-        CK(cudaStreamWaitEvent(cs, chunk_event(ctx, c), 0));
-        gemv_chunk(c);
       }
     } else {
       r2c_series(0, n_in);

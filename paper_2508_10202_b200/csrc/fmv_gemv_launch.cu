@@ -153,9 +153,39 @@ void sbgemv_staged_v(fmv_ctx* ctx, GemvPlan& gp) {
   }
 }
 
+// Small (Conj)Trans problems (short columns, a few MB in all): the
+// latency-oriented k_sbgemv_small (FMV_SBGEMV_SMALL=0 disables).
+template <int MODE, class E, class O>
+bool sbgemv_small_t(fmv_ctx* ctx, GemvPlan& gp) {
+  if constexpr (MODE == GM_N) {
+    return false;
+  } else {
+    constexpr int VMAX = (int)(16 / sizeof(E));
+    const GemvParams& p = gp.p;
+    const size_t bytes = (size_t)p.batch * p.n * p.m * sizeof(E);
+    if (p.m > 64 || bytes > ((size_t)env_int("FMV_SBGEMV_SMALL_MB", 32) << 20) || !env_int("FMV_SBGEMV_SMALL", 1))
+      return false;
+    const auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    const bool vec = VMAX > 1 && p.m % VMAX == 0 && p.lda % VMAX == 0 && p.sa % VMAX == 0 && al16(p.A);
+    const unsigned grid = (unsigned)((p.T + 127) / 128);
+    launch(ctx, 2, [&] {
+      if (vec) {
+        if constexpr (VMAX > 1) launch_pdl(k_sbgemv_small<MODE, E, O, VMAX>, dim3(grid), dim3(128), 0, ctx->stream, gp.p);
+      } else {
+        launch_pdl(k_sbgemv_small<MODE, E, O, 1>, dim3(grid), dim3(128), 0, ctx->stream, gp.p);
+      }
+    });
+    return true;
+  }
+}
+
 template <int MODE, class E, class O>
 void sbgemv_run_t(fmv_ctx* ctx, GemvPlan& gp, bool force_simple, int* used) {
   constexpr int VMAX = (int)(16 / sizeof(E));
+  if (!force_simple && sbgemv_small_t<MODE, E, O>(ctx, gp)) {
+    if (used) *used = 2;
+    return;
+  }
   // 16-byte row vectors need 16-byte aligned columns (and x for (Conj)Trans)
   const auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
   bool vec = VMAX > 1 && gp.p.lda % VMAX == 0 && gp.p.sa % VMAX == 0 && al16(gp.p.A);

@@ -537,7 +537,7 @@ bool block_gemv_run(fmv_ctx* ctx, int p2, int p3, int mode, const GemvArgs& a);
 constexpr int kBlockMax = 8;
 inline int block_max(bool fwd) { return fwd ? kBlockMax : 4; }
 #ifndef FMV_BLOCK_CONS
-#define FMV_BLOCK_CONS 512  // k_sbgemm_block consumer threads per CTA (+ one producer warp)
+#define FMV_BLOCK_CONS 416  // k_sbgemm_block consumer threads per CTA (+ one producer warp)
 #endif
 constexpr int kBlockConsumers = FMV_BLOCK_CONS;
 

@@ -31,7 +31,7 @@ namespace fmv {
 // One 16-warp CTA per SM with ~64 KB stages, as k_sbgemv: at C2 fp64 F K = 8
 // goes 2949 -> 3190 RHS/s against two 8-warp CTAs per SM (tools/ab_block.sh).
 #ifndef FMV_BLOCK_CONS
-#define FMV_BLOCK_CONS 512  // consumer threads per CTA (+ one producer warp)
+#define FMV_BLOCK_CONS 416  // consumer threads per CTA (+ one producer warp): 14 warps -> up to 128 registers (tools/bench_block.py)
 #endif
 #ifndef FMV_BLOCK_MINB
 #define FMV_BLOCK_MINB 1  // resident CTAs per SM
@@ -114,9 +114,17 @@ __global__ void __launch_bounds__(FMV_BLOCK_CONS + 32, FMV_BLOCK_MINB) k_sbgemm_
     const int g = t / p.RT;
     const bool active = g < p.G && r < p.m;
     constexpr bool kComp = !std::is_same<Acc, double2>::value;
+    // fp64: the four real products of each complex MAC go to four separate
+    // accumulators (re = rr - ii, im = ri + ir at the bin flush), so the 4K
+    // DFMAs of a column are independent: no DFMA -> DFMA dependency inside a
+    // column, which left the FP64 pipe ~41 % busy behind `wait` stalls.
+    constexpr bool kSplit = std::is_same<E, double2>::value;
     Acc acc[KR], cmp[KR];
+    double rr[kSplit ? KR : 1], ii[kSplit ? KR : 1], ri[kSplit ? KR : 1], ir[kSplit ? KR : 1];
 #pragma unroll
     for (int k = 0; k < KR; ++k) acc[k] = cmp[k] = Tr::zero();
+#pragma unroll
+    for (int k = 0; k < (kSplit ? KR : 1); ++k) rr[k] = ii[k] = ri[k] = ir[k] = 0.0;
     for (SegIter sg(c0, c1, p); sg.more(); sg.advance(p)) {
       sg.load(p);
       const int s = sg.s;
@@ -126,7 +134,29 @@ __global__ void __launch_bounds__(FMV_BLOCK_CONS + 32, FMV_BLOCK_MINB) k_sbgemm_
       // x slice r starts at its slot + the source's offset within 16 bytes
       const unsigned char* xbase = base + p.a_slot;
       mbar_wait_sleep(&full[s], sg.par);
-      if (active) {
+      if (active && kSplit) {
+        if constexpr (kSplit) {
+          const int cnt = (int)sg.cnt;
+          const E* Xs[KR];
+#pragma unroll
+          for (int k = 0; k < KR; ++k) {
+            const unsigned char* x0 = p.x + (sg.b * p.sx + k * p.sxr + sg.j) * es;
+            Xs[k] = reinterpret_cast<const E*>(xbase + k * p.xr_slot + (reinterpret_cast<uintptr_t>(x0) & 15));
+          }
+          for (int jj = g; jj < cnt; jj += p.G) {
+            const double2 a = As[(long)jj * p.lda + r];
+#pragma unroll
+            for (int k = 0; k < KR; ++k)
+              if (k < K) {
+                const double2 x = Xs[k][jj];
+                rr[k] = fma(a.x, x.x, rr[k]);
+                ii[k] = fma(a.y, x.y, ii[k]);
+                ri[k] = fma(a.x, x.y, ri[k]);
+                ir[k] = fma(a.y, x.x, ir[k]);
+              }
+          }
+        }
+      } else if (active) {
         const int cnt = (int)sg.cnt;
         Acc part[KR];
 #pragma unroll
@@ -156,6 +186,10 @@ __global__ void __launch_bounds__(FMV_BLOCK_CONS + 32, FMV_BLOCK_MINB) k_sbgemm_
         if (active) {
 #pragma unroll
           for (int k = 0; k < KR; ++k) {
+            if constexpr (kSplit) {
+              acc[k] = make_double2(rr[k] - ii[k], ri[k] + ir[k]);
+              rr[k] = ii[k] = ri[k] = ir[k] = 0.0;
+            }
             if (k < K) red[((long)g * K + k) * p.m + r] = kComp ? Tr::add(acc[k], cmp[k]) : acc[k];
             acc[k] = cmp[k] = Tr::zero();
           }

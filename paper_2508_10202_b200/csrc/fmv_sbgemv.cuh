@@ -680,4 +680,46 @@ __global__ void k_sbgemv_simple(const GemvParams p) {
   }
 }
 
+// Latency-oriented (Conj)Trans SBGEMV for small problems with short columns
+// (C4's m = 10 cells, a few MB in all): one thread per output y_b[j], flat
+// over batch*n so a single wave covers the GPU, the column read with
+// V-element 16-byte vector loads and x_b through the read-only cache. No TMA
+// ring or mbarriers: the whole call is one DRAM round trip plus the launch,
+// where the staged kernel's pipeline fill dominated (sbgemv_run_t picks it).
+template <int MODE, class E, class O, int V>
+__global__ void __launch_bounds__(128) k_sbgemv_small(const GemvParams p) {
+  using Tr = ET<E>;
+  using Acc = typename Tr::A;
+  struct alignas(16) Vec {
+    E v[V];
+  };
+  grid_dep_wait();
+  const long o = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= p.T) return;
+  const long b = o / p.n, j = o - b * p.n;
+  const E* col = reinterpret_cast<const E*>(p.A) + b * p.sa + j * p.lda;
+  const E* xb = reinterpret_cast<const E*>(p.x) + b * p.sx;
+  Acc a = Tr::zero();
+  if constexpr (V > 1) {
+    for (int i = 0; i < p.m; i += V) {
+      const uint4 raw = __ldg(reinterpret_cast<const uint4*>(col + i));
+      Vec w;
+      memcpy(&w, &raw, sizeof(Vec));
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const E xv = __ldg(xb + i + v);
+        if constexpr (MODE == GM_C) a = Tr::macc(a, w.v[v], xv);
+        else a = Tr::mac(a, w.v[v], xv);
+      }
+    }
+  } else {
+    for (int i = 0; i < p.m; ++i) {
+      const E xv = __ldg(xb + i);
+      if constexpr (MODE == GM_C) a = Tr::macc(a, __ldg(col + i), xv);
+      else a = Tr::mac(a, __ldg(col + i), xv);
+    }
+  }
+  reinterpret_cast<O*>(p.y)[b * p.sy + j] = out_cast<O>(a);
+}
+
 }  // namespace fmv

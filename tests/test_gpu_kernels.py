@@ -72,7 +72,7 @@ def test_gemv_reference_golden():
             xl, yl = (13, 7) if mode == 0 else (7, 13)
             for simple in (False, True):
                 y, used = F.gemv_batched(F.GemvMode(mode), dt, 7, 13, 3, 7, 91, A, xl, x, yl, force_simple=simple)
-                assert used == (1 if simple else 0)
+                assert used == (1 if simple else 2 if mode else 0)  # 2: small-problem (Conj)Trans kernel
                 assert rel(y, want) <= 16 * np.finfo(np.float32 if dt in "sc" else np.float64).eps * 7, (dt, mode)
 
 
@@ -134,6 +134,7 @@ def test_conjtrans_resident_x_matches_per_stage_x(monkeypatch):
     same bits as re-copying it with every stage, incl. tall columns (multi-warp
     per column) and pieces that start mid batch."""
     rng = np.random.default_rng(9)
+    monkeypatch.setenv("FMV_SBGEMV_SMALL", "0")  # (the staged kernel is the one under test)
     for m, n, b, dt in ((600, 3000, 3, "z"), (1000, 700, 2, "d"), (100, 5000, 4, "c"), (37, 900, 5, "z")):
         A = _rand(rng, m * n * b, dt)
         x = _rand(rng, m * b, dt)
@@ -143,3 +144,29 @@ def test_conjtrans_resident_x_matches_per_stage_x(monkeypatch):
             out[flag], used = F.gemv_batched(F.GemvMode.ConjTrans, dt, m, n, b, m, m * n, A, m, x, n)
             assert used == 0
         assert np.array_equal(out["0"], out["1"]), (m, n, b, dt)
+
+
+@pytest.mark.parametrize("dt", ["s", "d", "c", "z"])
+def test_small_conjtrans_kernel_vs_reference_and_staged(ref, monkeypatch, dt):
+    """The latency-oriented small-problem (Conj)Trans kernel (C4's m = 10,
+    n = 10^3, batch 100 cells): against the reference's naive GEMV and the
+    staged TMA kernel, with vector loads (m a multiple of the 16-byte width),
+    scalar loads (odd m, padded lda) and the real Trans path."""
+    rng = np.random.default_rng(12)
+    eps = np.finfo(np.float32 if dt in "sc" else np.float64).eps
+    for m, n, b, lda, mode in ((10, 1000, 100, 10, 2), (8, 333, 7, 8, 2), (13, 500, 9, 15, 2), (10, 1000, 100, 10, 1),
+                               (64, 129, 3, 64, 2)):
+        sa = lda * n
+        A = _rand(rng, b * sa, dt)
+        x = _rand(rng, b * m, dt)
+        want = np.zeros(b * n, dtype=A.dtype)
+        ref.gemv(0, mode, dt, m, n, b, lda, sa, A, m, x, n, want)
+        got, used = F.gemv_batched(F.GemvMode(mode), dt, m, n, b, lda, sa, A, m, x, n)
+        assert used == 2
+        scale = np.abs(A).max() * np.abs(x).max() * m
+        assert np.abs(got - want).max() / scale <= 16 * eps * m, (m, n, b, dt, mode)
+        monkeypatch.setenv("FMV_SBGEMV_SMALL", "0")
+        staged, used0 = F.gemv_batched(F.GemvMode(mode), dt, m, n, b, lda, sa, A, m, x, n)
+        monkeypatch.delenv("FMV_SBGEMV_SMALL")
+        assert used0 == 0
+        assert np.abs(got - staged).max() / scale <= 16 * eps * m

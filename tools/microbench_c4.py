@@ -39,9 +39,12 @@ def load_cublas():
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default="profiles/c4_microbench_r01")
+    ap.add_argument("--out", default="profiles/c4_microbench_r02")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--cold", type=int, default=2)
+    ap.add_argument("--ms", default="10,100,1000")
+    ap.add_argument("--ns", default="1000,10000,100000")
+    ap.add_argument("--dtypes", default="sdcz")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     ctx = F.Context(0)
@@ -56,10 +59,10 @@ def main():
     peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
     rows = []
     batch = 100
-    for dt in "sdcz":
+    for dt in a.dtypes:
         tdt, es = DT[dt]
-        for m in (10, 100, 1000):
-            for n in (1000, 10000, 100000):
+        for m in [int(v) for v in a.ms.split(",")]:
+            for n in [int(v) for v in a.ns.split(",")]:
                 abytes = m * n * batch * es
                 free, _ = torch.cuda.mem_get_info(dev)
                 if abytes + 64 * 2 ** 20 > 0.8 * free:
@@ -110,7 +113,7 @@ def main():
                                          ctypes.c_void_p(A.data_ptr()), m, ctypes.c_void_p(x.data_ptr()), n,
                                          ctypes.c_void_p(y.data_ptr()), 0, ctypes.byref(used)))
                 row = {"dtype": dt, "m": m, "n": n, "batch": batch, "ours_s": t_ours,
-                       "ours_gbs": F.effective_bandwidth(m, n, batch, es, t_ours), "kernel": "staged" if used.value == 0 else "simple"}
+                       "ours_gbs": F.effective_bandwidth(m, n, batch, es, t_ours), "kernel": {0: "staged", 1: "simple", 2: "small"}[used.value]}
                 if cb is not None:
                     t_cb = timeit(cublas)
                     ctx.synchronize()
