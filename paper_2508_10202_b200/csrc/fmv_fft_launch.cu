@@ -5,6 +5,8 @@
 #include "fmv_runtime.cuh"
 #include "fmv_fft.cuh"
 #include "fmv_fft_rt.cuh"
+#include "fmv_fft_pair.cuh"
+#include "fmv_fft_stream.cuh"
 
 namespace fmv {
 namespace rt {
@@ -77,6 +79,67 @@ inline FftPath fft_path() {  // (read per call: tests switch paths within one pr
 }
 #ifndef FMV_FFT_S64
 #define FMV_FFT_S64 2  // fp64 Nt = 1000 series per CTA of the register FFT kernels
+#endif
+// Big N = 1000 transforms of the matvec (>= 1024 series, zero-padded input /
+// first-half output) have three kernel sets: the one-shot one-butterfly-per-
+// thread k_r2c_reg / k_c2r_reg ("reg"), the paired-butterfly kernels
+// (fmv_fft_pair.cuh, "pair") and the persistent prefetching kernels
+// (fmv_fft_stream.cuh, "stream"). Defaults are the measured best at C2
+// (tools/tune_pair.py): fp64 r2c reg 47.9 / pair 50.2 /
+// stream 50.7 us, fp64 c2r 44.2 / 63.3 / 57.7, fp32 r2c 39.0 / 46.3 / 35.2,
+// fp32 c2r 39.4 / 35.5 / 41.4. (The fp32 stream r2c is faster by itself but
+// its F matvec is not: 0.6329 vs 0.6279 ms for dssdd -- the SBGEMV after it
+// runs slower.) FMV_FFT_BIG = reg | pair | stream forces one.
+enum BigFft { BF_REG, BF_PAIR, BF_STREAM };
+inline BigFft big_fft_kind(int N, long nseries, int nvalid, bool r2c, bool f64) {
+  if (N != 1000 || nvalid != N || nseries < 1024) return BF_REG;
+  const char* v = getenv("FMV_FFT_BIG");
+  if (v && *v) {
+    const std::string k = v;
+    return k == "reg" ? BF_REG : k == "pair" ? BF_PAIR : BF_STREAM;
+  }
+  return f64 || r2c ? BF_REG : BF_PAIR;
+}
+#ifndef FMV_STREAM_S64
+#define FMV_STREAM_S64 2
+#endif
+#ifndef FMV_STREAM_S32
+#define FMV_STREAM_S32 4
+#endif
+// register caps (__maxnreg__) of the stream kernels: r2c / c2r, fp64 / fp32
+#ifndef FMV_STREAM_R2C_R64
+#define FMV_STREAM_R2C_R64 64
+#endif
+#ifndef FMV_STREAM_C2R_R64
+#define FMV_STREAM_C2R_R64 80
+#endif
+#ifndef FMV_STREAM_R32
+#define FMV_STREAM_R32 64
+#endif
+// Resident CTAs per SM of a kernel at a block size / dynamic smem (cached).
+inline int occupancy(const void* fn, int block, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int, size_t>, int> cache;
+  const int dev = cur_device();
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_tuple(dev, fn, block, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem));
+  return cache[key] = std::max(1, n);
+}
+#ifndef FMV_PAIR_S64
+#define FMV_PAIR_S64 4
+#endif
+#ifndef FMV_PAIR_MINB64
+#define FMV_PAIR_MINB64 2
+#endif
+#ifndef FMV_PAIR_S32
+#define FMV_PAIR_S32 8
+#endif
+#ifndef FMV_PAIR_MINB32
+#define FMV_PAIR_MINB32 2
 #endif
 bool fft_reg_ok(int N) {
   return (N == 1000 || N == 100) && (fft_path() == FP_AUTO || fft_path() == FP_REG);
@@ -297,6 +360,43 @@ void r2c_reg_launch(fmv_ctx* ctx, const Tin* in, long in_ss, long nseries, int n
   });
 }
 
+template <int C0, int C1, int C2, class Tin, int S, int MINB>
+void r2c_pair_launch(fmv_ctx* ctx, const Tin* in, long in_ss, long nseries, void* out, long out_ks) {
+  using R = typename PT<C1>::real;
+  using C = typename CT<R>::c;
+  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, 2000, C1, 10));
+  bool vec = in_ss % 2 == 0;
+  if constexpr (sizeof(Tin) == 8) vec = vec && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  else if constexpr (sizeof(Tin) == 4) vec = vec && (reinterpret_cast<uintptr_t>(in) & 7) == 0;
+  else vec = false;
+  const long grid = (nseries + S - 1) / S;
+  constexpr size_t smem = pair_smem<C, S>();
+  auto kern = k_r2c_pair<C0, C1, C2, Tin, S, MINB>;
+  prep_smem((const void*)kern, smem);
+  prep_carveout((const void*)kern);
+  launch(ctx, 0, [&] {
+    launch_pdl(kern, dim3((unsigned)grid), dim3(S * 50), smem, ctx->stream, in, in_ss, nseries, vec,
+               static_cast<typename PT<C2>::cplx*>(out), out_ks, tw);
+  });
+}
+
+template <int C0, int C1, int C2, int S, int MAXR>
+void r2c_stream_launch(fmv_ctx* ctx, const double* in, long nseries, void* out, long out_ks) {
+  using R = typename PT<C1>::real;
+  using C = typename CT<R>::c;
+  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, 2000, C1, 10));
+  constexpr size_t smem = r2c_stream_smem<C, S>();
+  auto kern = k_r2c_stream<C0, C1, C2, S, MAXR>;
+  prep_smem((const void*)kern, smem);
+  prep_carveout((const void*)kern);
+  const long ntiles = (nseries + S - 1) / S;
+  const long grid = std::min(ntiles, (long)occupancy((const void*)kern, S * 100, smem) * sm_count(ctx->device));
+  launch(ctx, 0, [&] {
+    launch_pdl(kern, dim3((unsigned)grid), dim3(S * 100), smem, ctx->stream, in, nseries,
+               static_cast<typename PT<C2>::cplx*>(out), out_ks, tw);
+  });
+}
+
 template <int C0, int C1, int C2, class Tin>
 void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, int N, int nvalid, void* out,
            long out_ks, long out_ss) {
@@ -306,6 +406,21 @@ void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, in
   if constexpr (tin_ok) {
     if (in_ts == 1 && out_ss == 1 && fft_reg_ok(N)) {
       constexpr bool f64 = sizeof(R) == 8;
+      if constexpr (sizeof(Tin) == 8) {
+        if (big_fft_kind(N, nseries, nvalid, true, f64) == BF_STREAM && in_ss == N &&
+            (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+          r2c_stream_launch<C0, C1, C2, f64 ? FMV_STREAM_S64 : FMV_STREAM_S32, f64 ? FMV_STREAM_R2C_R64 : FMV_STREAM_R32>(
+              ctx, in, nseries, out, out_ks);
+          return;
+        }
+      }
+      if (big_fft_kind(N, nseries, nvalid, true, f64) == BF_PAIR) {
+        if constexpr (f64)
+          r2c_pair_launch<C0, C1, C2, Tin, FMV_PAIR_S64, FMV_PAIR_MINB64>(ctx, in, in_ss, nseries, out, out_ks);
+        else
+          r2c_pair_launch<C0, C1, C2, Tin, FMV_PAIR_S32, FMV_PAIR_MINB32>(ctx, in, in_ss, nseries, out, out_ks);
+        return;
+      }
       // (fp64: one series per CTA for small batches -- more CTAs for the 100-series transforms)
       if (N == 1000 && f64 && nseries < 1024)
         r2c_reg_launch<C0, C1, C2, Tin, 10, 3, 1>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
@@ -386,6 +501,40 @@ void c2r_reg_launch(fmv_ctx* ctx, const void* in, long in_ks, long nseries, int 
   });
 }
 
+template <int C3, int C4, class Tout, int S, int MINB>
+void c2r_pair_launch(fmv_ctx* ctx, const void* in, long in_ks, long nseries, Tout* out, long out_ss) {
+  using C = typename PT<C3>::cplx;
+  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, 2000, C3, 10));
+  const bool vec = sizeof(Tout) == 8 && (out_ss % 2 == 0) && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  const long grid = (nseries + S - 1) / S;
+  constexpr size_t smem = pair_smem<C, S>();
+  auto kern = k_c2r_pair<C3, C4, Tout, S, MINB>;
+  prep_smem((const void*)kern, smem);
+  prep_carveout((const void*)kern);
+  launch(ctx, 3, [&] {
+    launch_pdl(kern, dim3((unsigned)grid), dim3(S * 50), smem, ctx->stream, static_cast<const C*>(in), in_ks,
+               nseries, vec, out, out_ss, tw);
+  });
+}
+
+template <int C3, int C4, class Tout, int S, int MAXR>
+void c2r_stream_launch(fmv_ctx* ctx, const void* in, long in_ks, long nseries, Tout* out, long out_ss) {
+  using C = typename PT<C3>::cplx;
+  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, 2000, C3, 10));
+  const bool vec = sizeof(Tout) == 8 && (out_ss % 2 == 0) && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  using Cr = typename CT<typename PT<C3>::real>::c;
+  constexpr size_t smem = c2r_stream_smem<Cr, S>();
+  auto kern = k_c2r_stream<C3, C4, Tout, S, MAXR>;
+  prep_smem((const void*)kern, smem);
+  prep_carveout((const void*)kern);
+  const long ntiles = (nseries + S - 1) / S;
+  const long grid = std::min(ntiles, (long)occupancy((const void*)kern, S * 100, smem) * sm_count(ctx->device));
+  launch(ctx, 3, [&] {
+    launch_pdl(kern, dim3((unsigned)grid), dim3(S * 100), smem, ctx->stream, static_cast<const C*>(in), in_ks,
+               nseries, vec, out, out_ss, tw);
+  });
+}
+
 template <int C3, int C4, class Tout>
 void c2r_global(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, int N, int nout, Tout* out,
                 long out_ss) {
@@ -417,6 +566,16 @@ void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, i
   using C = typename PT<C3>::cplx;
   if (in_ss == 1 && fft_reg_ok(N)) {
     constexpr bool f64 = C3 == PD;
+    if (big_fft_kind(N, nseries, nout, false, f64) == BF_STREAM) {
+      c2r_stream_launch<C3, C4, Tout, f64 ? FMV_STREAM_S64 : FMV_STREAM_S32, f64 ? FMV_STREAM_C2R_R64 : FMV_STREAM_R32>(
+          ctx, in, in_ks, nseries, out, out_ss);
+      return;
+    }
+    if (big_fft_kind(N, nseries, nout, false, f64) == BF_PAIR) {
+      if constexpr (f64) c2r_pair_launch<C3, C4, Tout, FMV_PAIR_S64, FMV_PAIR_MINB64>(ctx, in, in_ks, nseries, out, out_ss);
+      else c2r_pair_launch<C3, C4, Tout, FMV_PAIR_S32, FMV_PAIR_MINB32>(ctx, in, in_ks, nseries, out, out_ss);
+      return;
+    }
     if (N == 1000)
     {
       // fp32: 8 series per CTA for the big (Nm-series) transform, 2 for the small
