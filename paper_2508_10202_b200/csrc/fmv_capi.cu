@@ -145,32 +145,57 @@ struct HostIO {
   };
   std::vector<Pending> pending;  // staged output chunks not yet copied to h_out
 
-  // host bytes [off, off + bytes) of the input -> device dst
+  // host bytes [off, off + bytes) of the input -> device dst. A pageable
+  // source is staged in ~2 MB pieces, each piece's DMA issued as soon as it
+  // is staged, so the copy engine streams while the host copies the next
+  // piece (one whole-chunk memcpy before the DMA serialized the two:
+  // F 2.7 ms -> DESIGN.md §3.5).
   void h2d(fmv_ctx* ctx, void* dst, size_t off, size_t bytes, cudaStream_t s) const {
     const unsigned char* src = static_cast<const unsigned char*>(h_in) + off;
-    if (pin_in) {
-      parallel_memcpy(pin_in + off, src, bytes);
-      src = pin_in + off;
+    if (!pin_in) {
+      copy_async(ctx, 0, dst, src, bytes, cudaMemcpyHostToDevice, s);
+      return;
     }
-    copy_async(ctx, 0, dst, src, bytes, cudaMemcpyHostToDevice, s);
+    const size_t piece = (size_t)env_int("FMV_STAGE_PIECE_KB", 2048) << 10;
+    for (size_t o = 0; o < bytes; o += piece) {
+      const size_t b = std::min(piece, bytes - o);
+      parallel_memcpy(pin_in + off + o, src + o, b);
+      copy_async(ctx, 0, static_cast<unsigned char*>(dst) + o, pin_in + off + o, b, cudaMemcpyHostToDevice, s);
+    }
   }
-  // device src -> output doubles [off, off + count); staged chunks complete in drain()
+  // device src -> output doubles [off, off + count); staged chunks complete in
+  // drain(). A pageable destination is drained in ~2 MB pieces, each with its
+  // own event, so the host copy of one piece overlaps the DMA of the next.
+  fmv_ctx* ev_ctx = nullptr;
+  size_t last_pieces = 0;  // pieces of the newest d2h call
   void d2h(fmv_ctx* ctx, size_t off, const double* src, size_t count, cudaStream_t s, cudaEvent_t ev) {
     if (!pin_out) {
       copy_async(ctx, 4, h_out + off, src, count * sizeof(double), cudaMemcpyDeviceToHost, s);
       return;
     }
-    copy_async(ctx, 4, pin_out + off, src, count * sizeof(double), cudaMemcpyDeviceToHost, s);
-    CK(cudaEventRecord(ev, s));
-    pending.push_back({off, count, ev});
+    (void)ev;
+    ev_ctx = ctx;
+    const size_t piece = std::max<size_t>(1, ((size_t)env_int("FMV_STAGE_PIECE_KB", 2048) << 10) / sizeof(double));
+    last_pieces = 0;
+    for (size_t o = 0; o < count; o += piece) {
+      const size_t c = std::min(piece, count - o);
+      copy_async(ctx, 4, pin_out + off + o, src + o, c * sizeof(double), cudaMemcpyDeviceToHost, s);
+      cudaEvent_t e = ctx->ev();
+      CK(cudaEventRecord(e, s));
+      pending.push_back({off + o, c, e});
+      ++last_pieces;
+    }
   }
-  // Copy staged output chunks to h_out, all but the newest `keep`.
-  void drain(size_t keep = 0) {
+  // Copy staged output pieces to h_out: all but those of the newest d2h call
+  // (newest = true), or all of them.
+  void drain(bool all_but_newest = false) {
+    const size_t keep = all_but_newest ? last_pieces : 0;
     while (pending.size() > keep) {
       const Pending q = pending.front();
       pending.erase(pending.begin());
       CK(cudaEventSynchronize(q.ev));
       parallel_memcpy(h_out + q.off, pin_out + q.off, q.count * sizeof(double));
+      ev_ctx->ev_pool.push_back(q.ev);
     }
   }
 };
@@ -325,7 +350,7 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
         const long j0 = chunk_edge(n, c, C), j1 = chunk_edge(n, c + 1, C);
         CK(cudaStreamWaitEvent(ks, chunk_event(ctx, c), 0));
         hio->d2h(ctx, j0 * nt, out + j0 * nt, (size_t)(j1 - j0) * nt, ks, chunk_event(ctx, 16 + c));
-        hio->drain(1);  // the previous staged chunk's host copy overlaps this chunk's SBGEMV
+        hio->drain(true);  // the previous staged chunk's host copy overlaps this chunk's SBGEMV
       };
       for (int c = 0; c < C; ++c) {
         const long j0 = chunk_edge(n, c, C), j1 = chunk_edge(n, c + 1, C);

@@ -73,6 +73,24 @@ int main() {
                   host / R * 1e3);
     }
   }
+  {  // pinning the caller's pageable buffer per call: register + DMA + unregister
+    const int R = 5;
+    double treg = 0, tdma = 0, tun = 0;
+    for (int r = 0; r < R; ++r) {
+      const double a = now();
+      cudaHostRegister(src.data(), bytes, cudaHostRegisterReadOnly);
+      const double b = now();
+      cudaMemcpy(dev, src.data(), bytes, cudaMemcpyHostToDevice);
+      const double c = now();
+      cudaHostUnregister(src.data());
+      const double d = now();
+      treg += b - a;
+      tdma += c - b;
+      tun += d - c;
+    }
+    std::printf(", \"register_ms\": %.3f, \"registered_h2d_ms\": %.3f, \"unregister_ms\": %.3f", treg / R * 1e3,
+                tdma / R * 1e3, tun / R * 1e3);
+  }
   {
     const int R = 10;
     double sink = 0;
