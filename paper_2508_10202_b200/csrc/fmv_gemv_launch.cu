@@ -298,9 +298,9 @@ bool plan_block(GemvPlan& gp, int mode, size_t es, size_t accsz, int KR) {
   return gp.smem <= 227 * 1024 && (long)(p.Jc - 1) * p.lda * (long)es + p.m * (long)es <= 96 * 1024;
 }
 
-template <int MODE, class E, class O, int KR, int LPC>
+template <int MODE, class E, class O, int KR, int LPC, int KX = 0, int XR = 0>
 void sbgemm_block_launch_t(fmv_ctx* ctx, GemvPlan& gp) {
-  auto kern = k_sbgemm_block<MODE, E, O, KR, LPC>;
+  auto kern = k_sbgemm_block<MODE, E, O, KR, LPC, KX, XR>;
   prep_smem((const void*)kern, gp.smem);
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, gp.block, gp.smem));
@@ -324,6 +324,21 @@ bool sbgemm_block_t(fmv_ctx* ctx, GemvPlan& gp) {
   // ConjTrans lanes per column: 8 for columns up to 128 elements, else a warp
   constexpr int L1 = MODE == GM_N ? 0 : 8, L2 = MODE == GM_N ? 0 : 32;
   const bool wide = MODE != GM_N && gp.p.m > 128;
+  if constexpr (MODE == GM_N && std::is_same<E, double2>::value) {
+    // exact-K variant with a fixed 1 KB x-slice stride (stages of <= 62 columns)
+    constexpr int XR = 1024;
+    GemvParams& q = gp.p;
+    if ((K == 8 || K == 4) && K == KR && q.xr_slot <= XR && env_int("FMV_BLOCK_EXACT", 1)) {
+      const size_t grow = (size_t)q.nstage * KR * (XR - q.xr_slot);
+      if (gp.smem + grow <= 227 * 1024) {
+        q.xr_slot = XR;
+        gp.smem += grow;
+        if (K == 8) sbgemm_block_launch_t<MODE, E, O, 8, L1, 8, XR>(ctx, gp);
+        else sbgemm_block_launch_t<MODE, E, O, 4, L1, 4, XR>(ctx, gp);
+        return true;
+      }
+    }
+  }
   if (KR == 2) wide ? sbgemm_block_launch_t<MODE, E, O, 2, L2>(ctx, gp) : sbgemm_block_launch_t<MODE, E, O, 2, L1>(ctx, gp);
   else if (KR == 4) wide ? sbgemm_block_launch_t<MODE, E, O, 4, L2>(ctx, gp) : sbgemm_block_launch_t<MODE, E, O, 4, L1>(ctx, gp);
   else wide ? sbgemm_block_launch_t<MODE, E, O, 8, L2>(ctx, gp) : sbgemm_block_launch_t<MODE, E, O, 8, L1>(ctx, gp);

@@ -36,7 +36,12 @@ namespace fmv {
 #ifndef FMV_BLOCK_MINB
 #define FMV_BLOCK_MINB 1  // resident CTAs per SM
 #endif
-template <int MODE, class E, class O, int KR, int LPC>
+// KX > 0 (NoTrans fp64 only): exactly KX = KR right-hand sides and x slices
+// XR bytes apart in shared memory, both compile-time -- the column loop then
+// has no per-RHS predicates and every x read is one LDS.128 at an immediate
+// offset from a single per-column base (the runtime-K loop spent ~30
+// integer / predicate instructions per 32 DFMAs on this).
+template <int MODE, class E, class O, int KR, int LPC, int KX = 0, int XR = 0>
 __global__ void __launch_bounds__(FMV_BLOCK_CONS + 32, FMV_BLOCK_MINB) k_sbgemm_block(const GemvParams p) {
   using Tr = ET<E>;
   using Acc = typename Tr::A;
@@ -143,17 +148,40 @@ __global__ void __launch_bounds__(FMV_BLOCK_CONS + 32, FMV_BLOCK_MINB) k_sbgemm_
             const unsigned char* x0 = p.x + (sg.b * p.sx + k * p.sxr + sg.j) * es;
             Xs[k] = reinterpret_cast<const E*>(xbase + k * p.xr_slot + (reinterpret_cast<uintptr_t>(x0) & 15));
           }
-          for (int jj = g; jj < cnt; jj += p.G) {
-            const double2 a = As[(long)jj * p.lda + r];
+          if constexpr (KX > 0 && XR > 0) {
+            static_assert(KX == KR, "exact-K variant");
+            // double2 slices are 16-byte aligned: Xs[k] = Xs[0] + k*XR
+            const unsigned char* xp = reinterpret_cast<const unsigned char*>(Xs[0]) + (long)g * 16;
+            const unsigned char* ap = reinterpret_cast<const unsigned char*>(As) + ((long)g * p.lda + r) * 16;
+            const long astep = (long)p.G * p.lda * 16;
+            const int xstep = p.G * 16;
+#pragma unroll(KX >= 8 ? 1 : 2)
+            for (int jj = g; jj < cnt; jj += p.G) {
+              const double2 a = *reinterpret_cast<const double2*>(ap);
 #pragma unroll
-            for (int k = 0; k < KR; ++k)
-              if (k < K) {
-                const double2 x = Xs[k][jj];
+              for (int k = 0; k < KX; ++k) {
+                const double2 x = *reinterpret_cast<const double2*>(xp + k * XR);
                 rr[k] = fma(a.x, x.x, rr[k]);
                 ii[k] = fma(a.y, x.y, ii[k]);
                 ri[k] = fma(a.x, x.y, ri[k]);
                 ir[k] = fma(a.y, x.x, ir[k]);
               }
+              ap += astep;
+              xp += xstep;
+            }
+          } else {
+            for (int jj = g; jj < cnt; jj += p.G) {
+              const double2 a = As[(long)jj * p.lda + r];
+#pragma unroll
+              for (int k = 0; k < KR; ++k)
+                if (k < K) {
+                  const double2 x = Xs[k][jj];
+                  rr[k] = fma(a.x, x.x, rr[k]);
+                  ii[k] = fma(a.y, x.y, ii[k]);
+                  ri[k] = fma(a.x, x.y, ri[k]);
+                  ir[k] = fma(a.y, x.x, ir[k]);
+                }
+            }
           }
         }
       } else if (active) {
