@@ -639,23 +639,37 @@ __global__ void __launch_bounds__(128) k_sbgemv_small(const GemvParams p) {
   const E* col = reinterpret_cast<const E*>(p.A) + b * p.sa + j * p.lda;
   const E* xb = reinterpret_cast<const E*>(p.x) + b * p.sx;
   Acc a = Tr::zero();
-  if constexpr (V > 1) {
-    for (int i = 0; i < p.m; i += V) {
-      const uint4 raw = __ldg(reinterpret_cast<const uint4*>(col + i));
-      Vec w;
-      memcpy(&w, &raw, sizeof(Vec));
+  // The column is read in groups of GR 16-byte loads that are all issued
+  // before the first FMA: after an L2 flush each load is a DRAM round trip,
+  // and a rolled (or load/FMA-interleaved) loop serialized them.
+  constexpr int GR = V > 1 ? 8 : 16;
+  for (int i0 = 0; i0 < p.m; i0 += GR * V) {
+    Vec w[GR];
+    E xv[GR * V];  // x_b too: after a flush it is a DRAM miss as well
+#pragma unroll
+    for (int g = 0; g < GR; ++g) {
+      const int i = i0 + g * V;
+      if (i < p.m) {
+        if constexpr (V > 1) {
+          const uint4 raw = __ldg(reinterpret_cast<const uint4*>(col + i));
+          memcpy(&w[g], &raw, sizeof(Vec));
+        } else {
+          w[g].v[0] = __ldg(col + i);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if (i + v < p.m) xv[g * V + v] = __ldg(xb + i + v);
+    }
+#pragma unroll
+    for (int g = 0; g < GR; ++g) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        const E xv = __ldg(xb + i + v);
-        if constexpr (MODE == GM_C) a = Tr::macc(a, w.v[v], xv);
-        else a = Tr::mac(a, w.v[v], xv);
+        if (i0 + g * V + v < p.m) {
+          if constexpr (MODE == GM_C) a = Tr::macc(a, w[g].v[v], xv[g * V + v]);
+          else a = Tr::mac(a, w[g].v[v], xv[g * V + v]);
+        }
       }
-    }
-  } else {
-    for (int i = 0; i < p.m; ++i) {
-      const E xv = __ldg(xb + i);
-      if constexpr (MODE == GM_C) a = Tr::macc(a, __ldg(col + i), xv);
-      else a = Tr::mac(a, __ldg(col + i), xv);
     }
   }
   reinterpret_cast<O*>(p.y)[b * p.sy + j] = out_cast<O>(a);
