@@ -629,7 +629,7 @@ struct IPow<0, RX> {
 // Phases 1-2 + reorder (as k_r2c) for SOTI input in[s*in_ss + t] and TOSI
 // output out[k*out_ks + s]; S series per CTA.
 template <int C0, int C1, int C2, class Tin, int RX, int NP, int S>
-__global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::NR <= 256 ? 5 : 2)
+__global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, RX >= 16 ? 2 : S * RegPlan<RX, NP>::NR <= 256 ? 5 : 2)
     k_r2c_reg(const Tin* __restrict__ in, long in_ss, long nseries, int nvalid, bool vec,
               typename PT<C2>::cplx* __restrict__ out, long out_ks,
               const typename CT<typename PT<C1>::real>::c* __restrict__ tw) {
@@ -708,7 +708,7 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::
 // Phases 4-5 + reorder (as k_c2r) for TOSI input in[k*in_ks + s] and SOTI
 // output out[s*out_ss + t], t < nout; S series per CTA.
 template <int C3, int C4, class Tout, int RX, int NP, int S>
-__global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, S * RegPlan<RX, NP>::NR <= 256 ? 5 : 2)
+__global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, RX >= 16 ? 2 : S * RegPlan<RX, NP>::NR <= 256 ? 5 : 2)
     k_c2r_reg(const typename PT<C3>::cplx* __restrict__ in, long in_ks, long nseries, int nout, bool vec,
               Tout* __restrict__ out, long out_ss, const typename PT<C3>::cplx* __restrict__ tw) {
   using R = typename PT<C3>::real;

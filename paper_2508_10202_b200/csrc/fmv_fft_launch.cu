@@ -142,7 +142,7 @@ inline int occupancy(const void* fn, int block, size_t smem) {
 #define FMV_PAIR_MINB32 2
 #endif
 bool fft_reg_ok(int N) {
-  return (N == 1000 || N == 100) && (fft_path() == FP_AUTO || fft_path() == FP_REG);
+  return (N == 1000 || N == 100 || N == 512 || N == 4096) && (fft_path() == FP_AUTO || fft_path() == FP_REG);
 }
 
 // Legacy two-buffer capacity: S = 1 series of 2 (N + 1) complex in <= 200 KB.
@@ -404,7 +404,7 @@ void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, in
   using C = typename CT<R>::c;
   constexpr bool tin_ok = sizeof(Tin) == 8 || (sizeof(Tin) == 4 && C0 == PS) || (sizeof(Tin) == 2 && C0 == PH);
   if constexpr (tin_ok) {
-    if (in_ts == 1 && out_ss == 1 && fft_reg_ok(N)) {
+    if (in_ts == 1 && out_ss == 1 && fft_reg_ok(N) && (N == 1000 || N == 100 || sizeof(Tin) == 8)) {
       constexpr bool f64 = sizeof(R) == 8;
       if constexpr (sizeof(Tin) == 8) {
         if (big_fft_kind(N, nseries, nvalid, true, f64) == BF_STREAM && in_ss == N &&
@@ -420,6 +420,14 @@ void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, in
         else
           r2c_pair_launch<C0, C1, C2, Tin, FMV_PAIR_S32, FMV_PAIR_MINB32>(ctx, in, in_ss, nseries, out, out_ks);
         return;
+      }
+      // N = 8^3 and 16^3: the same kernel with radix-8 / radix-16 passes
+      if (N == 512 || N == 4096) {
+        if constexpr (sizeof(Tin) == 8) {
+          if (N == 512) r2c_reg_launch<C0, C1, C2, Tin, 8, 3, 4>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
+          else r2c_reg_launch<C0, C1, C2, Tin, 16, 3, 1>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
+          return;
+        }
       }
       // (fp64: one series per CTA for small batches -- more CTAs for the 100-series transforms)
       if (N == 1000 && f64 && nseries < 1024)
@@ -574,6 +582,14 @@ void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, i
     if (big_fft_kind(N, nseries, nout, false, f64) == BF_PAIR) {
       if constexpr (f64) c2r_pair_launch<C3, C4, Tout, FMV_PAIR_S64, FMV_PAIR_MINB64>(ctx, in, in_ks, nseries, out, out_ss);
       else c2r_pair_launch<C3, C4, Tout, FMV_PAIR_S32, FMV_PAIR_MINB32>(ctx, in, in_ks, nseries, out, out_ss);
+      return;
+    }
+    if (N == 512) {
+      c2r_reg_launch<C3, C4, Tout, 8, 3, 4>(ctx, in, in_ks, nseries, nout, out, out_ss);
+      return;
+    }
+    if (N == 4096) {
+      c2r_reg_launch<C3, C4, Tout, 16, 3, 1>(ctx, in, in_ks, nseries, nout, out, out_ss);
       return;
     }
     if (N == 1000)
