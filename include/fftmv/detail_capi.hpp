@@ -8,10 +8,15 @@
 
 #include <cstdlib>
 
+#include <condition_variable>
+#include <exception>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <utility>
 
 #include "fftmv_cuda.h"
 
@@ -61,6 +66,92 @@ inline fmv_ctx* thread_ctx(int device = 0) {
   if (device < 0 || device >= 16) throw std::invalid_argument("fftmv: device index out of range");
   if (!h.c[device]) check(fmv_ctx_create(device, nullptr, &h.c[device]));
   return h.c[device];
+}
+
+// Grow-only pinned host buffer, one per host thread: the drop-in's large
+// matvec results land here by DMA and are copied into the returned
+// std::vector by the library's host threads (matvec.hpp run_pipeline).
+struct PinnedHost {
+  void* p = nullptr;
+  size_t n = 0;
+  void* ensure(size_t bytes) {
+    if (bytes > n) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      n = 0;
+      cuda_check(cudaHostAlloc(&p, bytes, cudaHostAllocDefault), "cudaHostAlloc");
+      n = bytes;
+    }
+    return p;
+  }
+  ~PinnedHost() {
+    if (p) (void)cudaFreeHost(p);
+  }
+};
+inline PinnedHost& thread_pinned_out() {
+  thread_local PinnedHost h;
+  return h;
+}
+
+// One persistent helper thread that runs a job while the caller does other
+// work. Persistent on purpose: glibc gives every thread its own malloc arena,
+// and a result vector freed by the caller goes back to the arena it came from,
+// so the next allocation on the same helper reuses it (a fresh thread per
+// call would page-fault a new 40 MB heap every time).
+class HelperThread {
+ public:
+  HelperThread() : th_([this] { loop(); }) {}
+  ~HelperThread() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    th_.join();
+  }
+  void start(std::function<void()> job) {
+    std::lock_guard<std::mutex> lk(mu_);
+    job_ = std::move(job);
+    done_ = false;
+    cv_.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return done_; });
+    if (err_) std::rethrow_exception(std::exchange(err_, nullptr));
+  }
+
+ private:
+  void loop() {
+    std::unique_lock<std::mutex> lk(mu_);
+    for (;;) {
+      cv_.wait(lk, [&] { return stop_ || job_; });
+      if (stop_) return;
+      auto job = std::move(job_);
+      job_ = nullptr;
+      lk.unlock();
+      std::exception_ptr e;
+      try {
+        job();
+      } catch (...) {
+        e = std::current_exception();
+      }
+      lk.lock();
+      err_ = e;
+      done_ = true;
+      cv_.notify_all();
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::function<void()> job_;
+  std::exception_ptr err_;
+  bool stop_ = false, done_ = true;
+  std::thread th_;
+};
+inline HelperThread& thread_helper() {
+  thread_local HelperThread h;
+  return h;
 }
 
 // Scoped device buffer.

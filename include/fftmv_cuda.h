@@ -205,6 +205,10 @@ uint64_t fmv_seed_stream(uint64_t seed, uint64_t stream);                       
 void fmv_uniform_fill(size_t count, uint64_t seed, double lo, double hi, double* out); /* random_fill.hpp:17-27 */
 int fmv_non_representable_fill(size_t count, uint64_t seed, double* out);           /* sweep.hpp:32-46 */
 int fmv_relative_error(size_t n, const double* x, const double* ref, double* out);  /* sweep.hpp:49-59 */
+/* memcpy of host memory by the library's host thread pool (the one that
+ * stages pageable matvec I/O): the drop-in's std::vector results are filled
+ * with it from a pinned buffer. No reference counterpart. */
+int fmv_host_copy(void* dst, const void* src, size_t bytes);
 
 #ifdef __cplusplus
 }

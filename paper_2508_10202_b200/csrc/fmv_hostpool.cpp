@@ -12,6 +12,8 @@
 #include <thread>
 #include <vector>
 
+#include "../../include/fftmv_cuda.h"
+
 namespace fmv {
 namespace rt {
 
@@ -112,3 +114,9 @@ void parallel_memcpy(void* dst, const void* src, size_t bytes) {
 
 }  // namespace rt
 }  // namespace fmv
+
+extern "C" int fmv_host_copy(void* dst, const void* src, size_t bytes) {
+  if ((!dst || !src) && bytes) return FMV_EINVAL;
+  if (bytes) fmv::rt::parallel_memcpy(dst, src, bytes);
+  return FMV_OK;
+}
