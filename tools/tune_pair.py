@@ -36,7 +36,7 @@ def call(kind, cfg):
 
 for cfg in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["ddddd", "dssdd", "sssss"]):
     outs = {}
-    for pair in ("reg", "pair", "stream"):
+    for pair in (os.environ.get("KINDS", "reg,pair,stream").split(",")):
         os.environ["FMV_FFT_BIG"] = pair
         for _ in range(3):
             call(0, cfg)
@@ -58,6 +58,6 @@ for cfg in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["ddddd", "dssdd", 
               f"F* c2r {c2r * 1e3:6.1f} us ({120.08e6 / c2r / 1e6:5.0f} GB/s)  F {sum(f_ms) / 20:.4f} ms  "
               f"F* {sum(a_ms) / 20:.4f} ms", flush=True)
     rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
-    for k in ("pair", "stream"):
+    for k in [x for x in outs if x != "reg"]:
         print(f"{cfg} {k} vs reg: F {rel(outs[k][0], outs['reg'][0]):.2e}  F* {rel(outs[k][1], outs['reg'][1]):.2e}",
               flush=True)
