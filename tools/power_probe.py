@@ -30,12 +30,23 @@ def l2_read():  # read 80 MB (clean lines), no writes
 def write8():  # 8 MB write
     with torch.cuda.stream(st):
         dirty[: 2 ** 20].fill_(2.0)
+flushbuf = torch.empty(20 * 2 ** 20, dtype=torch.float64, device="cuda")  # 160 MB (> L2), clean reads
+def l2_dirty_then_evict():  # 80 MB write, then read 160 MB of other data: the dirty lines leave L2 here
+    with torch.cuda.stream(st):
+        dirty.fill_(1.0)
+        sink.copy_(flushbuf.sum().reshape(1))
+def l2_dirty_then_sleep():  # 80 MB write, then ~100 us idle: does L2 write dirty lines back on its own?
+    with torch.cuda.stream(st):
+        dirty.fill_(1.0)
+        torch.cuda._sleep(200000)
 def tiny():
     with torch.cuda.stream(st):
         small.fill_(1.0)
 for name, seq in (("gemv only", [gemv]), ("F matvec", [fwd]), ("gemv + fp64 matmul", [gemv, fp64_burn]),
                   ("80 MB write + gemv", [l2_dirty, gemv]), ("tiny kernel + gemv", [tiny, gemv]),
-                  ("80 MB read + gemv", [l2_read, gemv]), ("8 MB write + gemv", [write8, gemv])):
+                  ("80 MB read + gemv", [l2_read, gemv]), ("8 MB write + gemv", [write8, gemv]),
+                  ("80MB write, 160MB read, gemv", [l2_dirty_then_evict, gemv]),
+                  ("80MB write, idle, gemv", [l2_dirty_then_sleep, gemv])):
     for _ in range(3):
         for f in seq: f()
     ctx.synchronize(); ctx.set_profiling(True); ctx.profile_read(True)
