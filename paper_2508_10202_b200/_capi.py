@@ -82,6 +82,7 @@ def lib() -> ctypes.CDLL:
         "fmv_uniform_fill": (None, [c_size_t, c_uint64, c_double, c_double, c_void_p]),
         "fmv_non_representable_fill": (c_int, [c_size_t, c_uint64, c_void_p]),
         "fmv_relative_error": (c_int, [c_size_t, c_void_p, c_void_p, POINTER(c_double)]),
+        "fmv_host_copy": (c_int, [c_void_p, c_void_p, c_size_t]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

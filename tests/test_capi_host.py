@@ -66,6 +66,24 @@ def test_relative_error():
         F.relative_error(x, x[:2])
 
 
+def test_host_copy():
+    """fmv_host_copy: the library's host-pool memcpy (fills the drop-in's result
+    vectors from its pinned buffer); sizes below and above the split threshold,
+    unaligned offsets, and the null-pointer error."""
+    import ctypes
+
+    L = F.lib()
+    rng = np.random.default_rng(3)
+    for n in (0, 1, 1000, 3 * 2 ** 20 + 7):
+        src = rng.integers(0, 255, n + 3, dtype=np.uint8)
+        dst = np.zeros(n + 3, dtype=np.uint8)
+        assert L.fmv_host_copy(dst.ctypes.data + 3, src.ctypes.data + 1, n) == 0
+        assert np.array_equal(dst[3:], src[1:n + 1])
+        assert not dst[:3].any()
+    assert L.fmv_host_copy(None, ctypes.c_void_p(src.ctypes.data), 16) == 1  # FMV_EINVAL
+    assert L.fmv_host_copy(None, None, 0) == 0
+
+
 def test_precision_config_grammar():
     c = F.parse_precision_config("dssdd")
     assert c.render() == "dssdd" and c[1] == F.Precision.Single and c[0] == F.Precision.Double
