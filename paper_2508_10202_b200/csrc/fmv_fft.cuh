@@ -493,10 +493,24 @@ __device__ __forceinline__ void cp_async(void* dst, const void* src, int bytes_v
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-template <int RX, int NP>
+template <int I, int RX>
+struct IPow {
+  static constexpr int v = RX * IPow<I - 1, RX>::v;
+};
+template <int RX>
+struct IPow<0, RX> {
+  static constexpr int v = 1;
+};
+
+// N = R0 * RX^(NP-1): a first pass of radix R0 (R0 divides RX; each thread
+// then does RX/R0 radix-R0 butterflies of it), the other NP-1 passes radix RX.
+// R0 = RX is the uniform plan (1000 = 10^3, 100 = 10^2, 512 = 8^3, 4096 = 16^3);
+// mixed ones cover 1024 = 4*16^2, 2048 = 8*16^2, 8192 = 2*16^3, 2000 = 2*10^3.
+template <int RX, int NP, int R0 = RX>
 struct RegPlan {
-  static constexpr int N = NP == 2 ? RX * RX : RX * RX * RX;
-  static constexpr int NR = N / RX;  // butterflies per series per pass
+  static_assert(RX % R0 == 0, "the first-pass radix must divide RX");
+  static constexpr int N = R0 * IPow<NP - 1, RX>::v;
+  static constexpr int NR = N / RX;  // threads per series (radix-RX butterflies per pass)
 };
 
 // Shared series stride: N rounded up so consecutive series start 128/S bytes
@@ -515,10 +529,10 @@ constexpr int reg_series_stride() {
 // One Stockham pass with Ns > 1 over the thread's butterfly: read, twiddle,
 // DFT, barrier, write, barrier.
 // Offset of pass Ns's twiddle table [q*Ns + k] behind the 2N-entry base table.
-template <int RX, int N, int Ns>
+template <int RX, int N, int Ns, int R0 = RX>
 constexpr int reg_tw_offset() {
   int off = 2 * N;
-  for (int ns = RX; ns < Ns; ns *= RX) off += RX * ns;
+  for (int ns = R0; ns < Ns; ns *= RX) off += RX * ns;
   return off;
 }
 
@@ -584,12 +598,12 @@ __device__ __forceinline__ void store_stride_rx(C* o, const C* v) {
   }
 }
 
-template <class R, int D, int RX, int N, int Ns>
+template <class R, int D, int RX, int N, int Ns, int R0 = RX>
 __device__ __forceinline__ void reg_pass(typename CT<R>::c* __restrict__ buf, int j, bool act,
                                          const typename CT<R>::c* __restrict__ tw) {
   using C = typename CT<R>::c;
   constexpr int NR = N / RX;
-  const C* __restrict__ twp = tw + reg_tw_offset<RX, N, Ns>();
+  const C* __restrict__ twp = tw + reg_tw_offset<RX, N, Ns, R0>();
   C v[RX];
   const int k = j % Ns;
   if (act) {
@@ -607,36 +621,45 @@ __device__ __forceinline__ void reg_pass(typename CT<R>::c* __restrict__ buf, in
   __syncthreads();
 }
 
-// Dynamic shared-memory bytes of the register kernels (host launch sizes).
-template <class C, int RX, int NP, int S>
-constexpr size_t r2c_reg_smem() {
-  return (size_t)S * reg_series_stride<C, RegPlan<RX, NP>::N, S>() * sizeof(C);
-}
-template <class C, int RX, int NP, int S>
-constexpr size_t c2r_reg_smem() {
-  return (size_t)S * reg_series_stride<C, RegPlan<RX, NP>::N + 1, S>() * sizeof(C);
+// Radix-RX passes with Ns = NS, NS*RX, ... up to NLAST (inclusive).
+template <class R, int D, int RX, int N, int R0, int NS, int NLAST>
+__device__ __forceinline__ void reg_passes(typename CT<R>::c* __restrict__ buf, int j, bool act,
+                                           const typename CT<R>::c* __restrict__ tw) {
+  if constexpr (NS <= NLAST) {
+    reg_pass<R, D, RX, N, NS, R0>(buf, j, act, tw);
+    reg_passes<R, D, RX, N, R0, NS * RX, NLAST>(buf, j, act, tw);
+  }
 }
 
-template <int I, int RX>
-struct IPow {
-  static constexpr int v = RX * IPow<I - 1, RX>::v;
-};
-template <int RX>
-struct IPow<0, RX> {
-  static constexpr int v = 1;
-};
+// Dynamic shared-memory bytes of the register kernels (host launch sizes).
+template <class C, int RX, int NP, int S, int R0 = RX>
+constexpr size_t r2c_reg_smem() {
+  return (size_t)S * reg_series_stride<C, RegPlan<RX, NP, R0>::N, S>() * sizeof(C);
+}
+template <class C, int RX, int NP, int S, int R0 = RX>
+constexpr size_t c2r_reg_smem() {
+  return (size_t)S * reg_series_stride<C, RegPlan<RX, NP, R0>::N + 1, S>() * sizeof(C);
+}
+// resident CTAs the register kernels ask for (register cap)
+template <int RX, int NP, int S, int R0>
+constexpr int reg_min_blocks() {
+  constexpr int T = S * RegPlan<RX, NP, R0>::NR;
+  if constexpr (R0 != RX && T >= 512) return 1;
+  return RX >= 16 ? 2 : T <= 256 ? 5 : 2;
+}
 
 // Phases 1-2 + reorder (as k_r2c) for SOTI input in[s*in_ss + t] and TOSI
 // output out[k*out_ks + s]; S series per CTA.
-template <int C0, int C1, int C2, class Tin, int RX, int NP, int S>
-__global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, RX >= 16 ? 2 : S * RegPlan<RX, NP>::NR <= 256 ? 5 : 2)
+template <int C0, int C1, int C2, class Tin, int RX, int NP, int S, int R0 = RX>
+__global__ void __launch_bounds__(S * RegPlan<RX, NP, R0>::NR, reg_min_blocks<RX, NP, S, R0>())
     k_r2c_reg(const Tin* __restrict__ in, long in_ss, long nseries, int nvalid, bool vec,
               typename PT<C2>::cplx* __restrict__ out, long out_ks,
               const typename CT<typename PT<C1>::real>::c* __restrict__ tw) {
   using R = typename PT<C1>::real;
   using C = typename CT<R>::c;
   using OutC = typename PT<C2>::cplx;
-  constexpr int N = RegPlan<RX, NP>::N, NR = RegPlan<RX, NP>::NR, T = S * NR;
+  constexpr int N = RegPlan<RX, NP, R0>::N, NR = RegPlan<RX, NP, R0>::NR, T = S * NR;
+  constexpr int U = RX / R0, NB = N / R0;  // pass-1 butterflies per thread, radix-R0 butterflies per series
   constexpr int SS = reg_series_stride<C, N, S>();
   extern __shared__ __align__(16) unsigned char reg_smem[];  // S * SS complex (dynamic: S*SS may exceed 48 KB)
   C* sbuf = reinterpret_cast<C*>(reg_smem);
@@ -647,13 +670,15 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, RX >= 16 ? 2 : S * Re
   C* buf = sbuf + s * SS;
   grid_dep_wait();  // (PDL)
 
-  // Pass 1 (Ns = 1, no twiddles): z[n] = v[2n] + i v[2n+1], n = j + q*NR.
+  // Pass 1 (Ns = 1, no twiddles): z[n] = v[2n] + i v[2n+1]; butterfly
+  // b = j + u*NR (u < U) reads n = b + r*NB (r < R0) into v[u*R0 + r]
+  // (R0 = RX: n = j + q*NR).
   {
     C v[RX];
     const Tin* p = in + (s0 + s) * in_ss;
 #pragma unroll
     for (int q = 0; q < RX; ++q) {
-      const int n = j + q * NR;
+      const int n = j + (q / R0) * NR + (q % R0) * NB;
       const int t0 = 2 * n;
       v[q] = C{R(0), R(0)};
       if (act && t0 < nvalid) {
@@ -675,13 +700,22 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, RX >= 16 ? 2 : S * Re
         v[q] = C{a, b};
       }
     }
-    butterfly<R, -1, RX>(v);
-    if (act) store_stride_rx<RX>(buf + j * RX, v);
+    if constexpr (R0 == RX) {
+      butterfly<R, -1, RX>(v);
+      if (act) store_stride_rx<RX>(buf + j * RX, v);
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) butterfly<R, -1, R0>(v + u * R0);
+      if (act) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int r = 0; r < R0; ++r) buf[(j + u * NR) * R0 + r] = v[u * R0 + r];
+      }
+    }
     __syncthreads();
   }
-  if constexpr (NP >= 3) reg_pass<R, -1, RX, N, RX>(buf, j, act, tw);
-  if constexpr (NP == 2) reg_pass<R, -1, RX, N, RX>(buf, j, act, tw);
-  else reg_pass<R, -1, RX, N, RX * RX>(buf, j, act, tw);
+  reg_passes<R, -1, RX, N, R0, R0, NR>(buf, j, act, tw);
 
   // Post-pass: X[k] = E[k] + w^k (-i) D[k] with E, D from Z[k] and
   // conj Z[N-k]. Bins k and N-k (k = 0 pairs with N) share the two loads.
@@ -707,13 +741,14 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, RX >= 16 ? 2 : S * Re
 
 // Phases 4-5 + reorder (as k_c2r) for TOSI input in[k*in_ks + s] and SOTI
 // output out[s*out_ss + t], t < nout; S series per CTA.
-template <int C3, int C4, class Tout, int RX, int NP, int S>
-__global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, RX >= 16 ? 2 : S * RegPlan<RX, NP>::NR <= 256 ? 5 : 2)
+template <int C3, int C4, class Tout, int RX, int NP, int S, int R0 = RX>
+__global__ void __launch_bounds__(S * RegPlan<RX, NP, R0>::NR, reg_min_blocks<RX, NP, S, R0>())
     k_c2r_reg(const typename PT<C3>::cplx* __restrict__ in, long in_ks, long nseries, int nout, bool vec,
               Tout* __restrict__ out, long out_ss, const typename PT<C3>::cplx* __restrict__ tw) {
   using R = typename PT<C3>::real;
   using C = typename CT<R>::c;
-  constexpr int N = RegPlan<RX, NP>::N, NR = RegPlan<RX, NP>::NR, T = S * NR;
+  constexpr int N = RegPlan<RX, NP, R0>::N, NR = RegPlan<RX, NP, R0>::NR, T = S * NR;
+  constexpr int U = RX / R0, NB = N / R0;
   constexpr int SS = reg_series_stride<C, N + 1, S>();
   extern __shared__ __align__(16) unsigned char reg_smem[];  // S * SS complex (dynamic: S*SS may exceed 48 KB)
   C* sbuf = reinterpret_cast<C*>(reg_smem);
@@ -744,28 +779,42 @@ __global__ void __launch_bounds__(S * RegPlan<RX, NP>::NR, RX >= 16 ? 2 : S * Re
       const C wj = __ldg(tw + j);
 #pragma unroll
       for (int q = 0; q < RX; ++q) {
-        const int n = j + q * NR;
+        const int n = j + (q / R0) * NR + (q % R0) * NB;  // (R0 = RX: j + q*NR)
         C A = buf[n], B = buf[N - n];  // X[n], X[N-n]
         A.x = A.x * inv_len;
         A.y = n == 0 ? R(0) : A.y * inv_len;  // Im(X0) = 0
         B.x = B.x * inv_len;
         B.y = n == 0 ? -R(0) : -(B.y * inv_len);  // conj; Im(XN) = 0 (sign of zero as cconj(0))
         C w;  // w^n = w^j * w^(q*N/RX); for RX = 10 the second factor is a constant
-        if constexpr (RX == 10) w = q == 0 ? wj : cmul(wj, half_turn10<R>(q));
+        if constexpr (RX == 10 && R0 == RX) w = q == 0 ? wj : cmul(wj, half_turn10<R>(q));
         else w = __ldg(tw + n);
         v[q] = cadd(cadd(A, B), cmuli<1>(cmul(C{w.x, -w.y}, csub(A, B))));
       }
-      butterfly<R, 1, RX>(v);
+      if constexpr (R0 == RX) {
+        butterfly<R, 1, RX>(v);
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) butterfly<R, 1, R0>(v + u * R0);
+      }
     }
     __syncthreads();
-    if (act) store_stride_rx<RX>(buf + j * RX, v);
+    if (act) {
+      if constexpr (R0 == RX) {
+        store_stride_rx<RX>(buf + j * RX, v);
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int r = 0; r < R0; ++r) buf[(j + u * NR) * R0 + r] = v[u * R0 + r];
+      }
+    }
     __syncthreads();
   }
-  if constexpr (NP >= 3) reg_pass<R, 1, RX, N, RX>(buf, j, act, tw);
+  reg_passes<R, 1, RX, N, R0, R0, NR / RX>(buf, j, act, tw);
   // Last pass (Ns = N/RX): out index j + q*NR, straight to global.
   {
     constexpr int Ns = NR;
-    const C* __restrict__ twp = tw + reg_tw_offset<RX, N, Ns>();
+    const C* __restrict__ twp = tw + reg_tw_offset<RX, N, Ns, R0>();
     C v[RX];
     if (act) {
 #pragma unroll

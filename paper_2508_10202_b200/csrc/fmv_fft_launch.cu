@@ -141,8 +141,13 @@ inline int occupancy(const void* fn, int block, size_t smem) {
 #ifndef FMV_PAIR_MINB32
 #define FMV_PAIR_MINB32 2
 #endif
+// Compile-time register plans beyond the matvec's 1000 / 100 (matvec path only):
+// 512 = 8^3, 4096 = 16^3, 1024 = 4*16^2, 2048 = 8*16^2, 8192 = 2*16^3, 2000 = 2*10^3.
+inline bool fft_reg_extra(int N) {
+  return N == 512 || N == 4096 || N == 1024 || N == 2048 || N == 8192 || N == 2000;
+}
 bool fft_reg_ok(int N) {
-  return (N == 1000 || N == 100 || N == 512 || N == 4096) && (fft_path() == FP_AUTO || fft_path() == FP_REG);
+  return (N == 1000 || N == 100 || fft_reg_extra(N)) && (fft_path() == FP_AUTO || fft_path() == FP_REG);
 }
 
 // Legacy two-buffer capacity: S = 1 series of 2 (N + 1) complex in <= 200 KB.
@@ -340,22 +345,30 @@ void r2c_global(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nserie
   }
 }
 
-template <int C0, int C1, int C2, class Tin, int RX, int NP, int S>
+// Twiddle table of a register plan (R0, RX, ..., RX): base + per-pass tables.
+inline const void* reg_plan_twiddles(int dev, int N, int prec, int RX, int NP, int R0) {
+  if (R0 == RX) return twiddles().get(dev, 2 * N, prec, RX);
+  std::vector<int> radices(NP, RX);
+  radices[0] = R0;
+  return twiddles().get_plan(dev, 2 * N, prec, radices);
+}
+
+template <int C0, int C1, int C2, class Tin, int RX, int NP, int S, int R0 = RX>
 void r2c_reg_launch(fmv_ctx* ctx, const Tin* in, long in_ss, long nseries, int nvalid, void* out, long out_ks) {
   using R = typename PT<C1>::real;
   using C = typename CT<R>::c;
-  const int N = RegPlan<RX, NP>::N;
-  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, 2 * N, C1, RX));
+  const int N = RegPlan<RX, NP, R0>::N;
+  const C* tw = static_cast<const C*>(reg_plan_twiddles(ctx->device, N, C1, RX, NP, R0));
   bool vec = (in_ss % 2 == 0) && (nvalid % 2 == 0);
   if constexpr (sizeof(Tin) == 8) vec = vec && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
   else if constexpr (sizeof(Tin) == 4) vec = vec && (reinterpret_cast<uintptr_t>(in) & 7) == 0;
   else vec = false;
   const long grid = (nseries + S - 1) / S;
-  constexpr size_t smem = r2c_reg_smem<C, RX, NP, S>();
-  prep_smem((const void*)k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>, smem);
-  prep_carveout((const void*)k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>);
+  constexpr size_t smem = r2c_reg_smem<C, RX, NP, S, R0>();
+  prep_smem((const void*)k_r2c_reg<C0, C1, C2, Tin, RX, NP, S, R0>, smem);
+  prep_carveout((const void*)k_r2c_reg<C0, C1, C2, Tin, RX, NP, S, R0>);
   launch(ctx, 0, [&] {
-    launch_pdl(k_r2c_reg<C0, C1, C2, Tin, RX, NP, S>, dim3((unsigned)grid), dim3(S * RegPlan<RX, NP>::NR), smem,
+    launch_pdl(k_r2c_reg<C0, C1, C2, Tin, RX, NP, S, R0>, dim3((unsigned)grid), dim3(S * RegPlan<RX, NP, R0>::NR), smem,
                ctx->stream, in, in_ss, nseries, nvalid, vec, static_cast<typename PT<C2>::cplx*>(out), out_ks, tw);
   });
 }
@@ -404,7 +417,7 @@ void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, in
   using C = typename CT<R>::c;
   constexpr bool tin_ok = sizeof(Tin) == 8 || (sizeof(Tin) == 4 && C0 == PS) || (sizeof(Tin) == 2 && C0 == PH);
   if constexpr (tin_ok) {
-    if (in_ts == 1 && out_ss == 1 && fft_reg_ok(N) && (N == 1000 || N == 100 || sizeof(Tin) == 8)) {
+    if (in_ts == 1 && out_ss == 1 && fft_reg_ok(N) && (!fft_reg_extra(N) || sizeof(Tin) == 8)) {
       constexpr bool f64 = sizeof(R) == 8;
       if constexpr (sizeof(Tin) == 8) {
         if (big_fft_kind(N, nseries, nvalid, true, f64) == BF_STREAM && in_ss == N &&
@@ -421,11 +434,15 @@ void r2c_t(fmv_ctx* ctx, const Tin* in, long in_ss, long in_ts, long nseries, in
           r2c_pair_launch<C0, C1, C2, Tin, FMV_PAIR_S32, FMV_PAIR_MINB32>(ctx, in, in_ss, nseries, out, out_ks);
         return;
       }
-      // N = 8^3 and 16^3: the same kernel with radix-8 / radix-16 passes
-      if (N == 512 || N == 4096) {
+      // the other compile-time plans (uniform radix-8 / 16, mixed R0 * RX^k)
+      if (fft_reg_extra(N)) {
         if constexpr (sizeof(Tin) == 8) {
           if (N == 512) r2c_reg_launch<C0, C1, C2, Tin, 8, 3, 4>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
-          else r2c_reg_launch<C0, C1, C2, Tin, 16, 3, 1>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
+          else if (N == 4096) r2c_reg_launch<C0, C1, C2, Tin, 16, 3, 1>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
+          else if (N == 1024) r2c_reg_launch<C0, C1, C2, Tin, 16, 3, 4, 4>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
+          else if (N == 2048) r2c_reg_launch<C0, C1, C2, Tin, 16, 3, 2, 8>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
+          else if (N == 8192) r2c_reg_launch<C0, C1, C2, Tin, 16, 4, 1, 2>(ctx, in, in_ss, nseries, nvalid, out, out_ks);
+          else r2c_reg_launch<C0, C1, C2, Tin, 10, 4, 1, 2>(ctx, in, in_ss, nseries, nvalid, out, out_ks);  // 2000
           return;
         }
       }
@@ -491,20 +508,20 @@ void r2c_dispatch(fmv_ctx* ctx, int c0, int c1, int c2, const Tin* in, long in_s
   fail(FMV_EINVAL, "r2c: unsupported precision combination");
 }
 
-template <int C3, int C4, class Tout, int RX, int NP, int S>
+template <int C3, int C4, class Tout, int RX, int NP, int S, int R0 = RX>
 void c2r_reg_launch(fmv_ctx* ctx, const void* in, long in_ks, long nseries, int nout, Tout* out, long out_ss) {
   using C = typename PT<C3>::cplx;
-  const int N = RegPlan<RX, NP>::N;
-  const C* tw = static_cast<const C*>(twiddles().get(ctx->device, 2 * N, C3, RX));
+  const int N = RegPlan<RX, NP, R0>::N;
+  const C* tw = static_cast<const C*>(reg_plan_twiddles(ctx->device, N, C3, RX, NP, R0));
   const bool vec = sizeof(Tout) == 8 && (out_ss % 2 == 0) && (nout % 2 == 0) &&
                    (reinterpret_cast<uintptr_t>(out) & 15) == 0;
   const long grid = (nseries + S - 1) / S;
   using Cr = typename CT<typename PT<C3>::real>::c;
-  constexpr size_t smem = c2r_reg_smem<Cr, RX, NP, S>();
-  prep_smem((const void*)k_c2r_reg<C3, C4, Tout, RX, NP, S>, smem);
-  prep_carveout((const void*)k_c2r_reg<C3, C4, Tout, RX, NP, S>);
+  constexpr size_t smem = c2r_reg_smem<Cr, RX, NP, S, R0>();
+  prep_smem((const void*)k_c2r_reg<C3, C4, Tout, RX, NP, S, R0>, smem);
+  prep_carveout((const void*)k_c2r_reg<C3, C4, Tout, RX, NP, S, R0>);
   launch(ctx, 3, [&] {
-    launch_pdl(k_c2r_reg<C3, C4, Tout, RX, NP, S>, dim3((unsigned)grid), dim3(S * RegPlan<RX, NP>::NR), smem,
+    launch_pdl(k_c2r_reg<C3, C4, Tout, RX, NP, S, R0>, dim3((unsigned)grid), dim3(S * RegPlan<RX, NP, R0>::NR), smem,
                ctx->stream, static_cast<const C*>(in), in_ks, nseries, nout, vec, out, out_ss, tw);
   });
 }
@@ -584,12 +601,13 @@ void c2r_t(fmv_ctx* ctx, const void* in, long in_ks, long in_ss, long nseries, i
       else c2r_pair_launch<C3, C4, Tout, FMV_PAIR_S32, FMV_PAIR_MINB32>(ctx, in, in_ks, nseries, out, out_ss);
       return;
     }
-    if (N == 512) {
-      c2r_reg_launch<C3, C4, Tout, 8, 3, 4>(ctx, in, in_ks, nseries, nout, out, out_ss);
-      return;
-    }
-    if (N == 4096) {
-      c2r_reg_launch<C3, C4, Tout, 16, 3, 1>(ctx, in, in_ks, nseries, nout, out, out_ss);
+    if (fft_reg_extra(N)) {
+      if (N == 512) c2r_reg_launch<C3, C4, Tout, 8, 3, 4>(ctx, in, in_ks, nseries, nout, out, out_ss);
+      else if (N == 4096) c2r_reg_launch<C3, C4, Tout, 16, 3, 1>(ctx, in, in_ks, nseries, nout, out, out_ss);
+      else if (N == 1024) c2r_reg_launch<C3, C4, Tout, 16, 3, 4, 4>(ctx, in, in_ks, nseries, nout, out, out_ss);
+      else if (N == 2048) c2r_reg_launch<C3, C4, Tout, 16, 3, 2, 8>(ctx, in, in_ks, nseries, nout, out, out_ss);
+      else if (N == 8192) c2r_reg_launch<C3, C4, Tout, 16, 4, 1, 2>(ctx, in, in_ks, nseries, nout, out, out_ss);
+      else c2r_reg_launch<C3, C4, Tout, 10, 4, 1, 2>(ctx, in, in_ks, nseries, nout, out, out_ss);  // 2000
       return;
     }
     if (N == 1000)
