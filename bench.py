@@ -199,7 +199,7 @@ def workload_config(world, cfg):
             "n_m_per_gpu": NM, "n_d": ND, "n_t": NT, "n_m_total": NM * world, "precision_config": cfg,
             "operator_bytes_per_gpu": (NT + 1) * ND * NM * 16,
             "l2": f"inputs larger than L2: the {(NT + 1) * ND * NM * 16 / 1e9:.1f} GB operator is streamed once per matvec",
-            "parallelism": f"1x{world} column partition" + (" (NCCL all-reduce / broadcast)" if world > 1 else ""),
+            "parallelism": f"1x{world} column partition" + (" (NCCL all-gather + fixed-tree reduce for F, broadcast for F*)" if world > 1 else ""),
             "matvec_unit": "one F or F* over an Nm=5000 shard; a distributed matvec on N GPUs = N units"}
 
 
