@@ -8,7 +8,7 @@ operator (Nm=5000, Nd=100, Nt=1000; 8.0 GB of complex128 bins per GPU), so
 the unit of work is one "shard-matvec" over an Nm=5000 column block. At N
 GPUs (torchrun, one rank per GPU) each rank holds its own Nm=5000 shard of an
 Nm=5000*N operator (weak scaling, partition.hpp 1 x p grid): one distributed
-F is N shard-matvecs + an NCCL all-reduce of d, one distributed F* is an NCCL
+F is N shard-matvecs + an NCCL all-gather of the partial d summed by a fixed tree, one distributed F* is an NCCL
 broadcast of d + N shard-matvecs.
 
 value   : shard-matvecs/s of the whole job, device-resident inputs (HBM).
