@@ -150,6 +150,30 @@ static void gpu_checks() {
     const auto ga = grid.adjoint(op, d, PrecisionConfig{});
     EXPECT(gf == F.output.f64 && ga == A.output.f64);
   }
+  // large results (>= 4 MB: F* at n_m*n_t = 600k) take the pinned-buffer + helper-thread path of
+  // run_pipeline; they must equal the C ABI's own host-I/O result bitwise, repeatedly (the helper's
+  // reused arena), and for F and F* with mixed configs too
+  {
+    const ProblemDims big(1000, 3, 600);
+    BlockColumn bcol(big, uniform_fill(big.n_t * big.n_d * big.n_m, seed_stream(7, 0)));
+    SpectralOperator bop = setup_operator(bcol, HostBins::Skip);
+    const auto bm = uniform_fill(big.n_m * big.n_t, seed_stream(7, 1));
+    const auto bd = uniform_fill(big.n_d * big.n_t, seed_stream(7, 2));
+    for (const char* c : {"ddddd", "dssdd"}) {
+      std::vector<double> want_a(big.n_m * big.n_t), want_f(big.n_d * big.n_t);
+      detail::check(fmv_matvec(detail::thread_ctx(0), bop.handle(), FMV_ADJOINT, c, bd.data(), want_a.data(), 0,
+                               nullptr));
+      detail::check(fmv_matvec(detail::thread_ctx(0), bop.handle(), FMV_FORWARD, c, bm.data(), want_f.data(), 0,
+                               nullptr));
+      for (int rep = 0; rep < 3; ++rep) {
+        auto ba = adjoint_matvec(bop, BlockVector::time_double(big.n_d, big.n_t, bd), parse_precision_config(c));
+        auto bf = forward_matvec(bop, BlockVector::time_double(big.n_m, big.n_t, bm), parse_precision_config(c));
+        EXPECT(ba.output.f64 == want_a);
+        EXPECT(bf.output.f64 == want_f);
+        EXPECT(ba.timings.total_s > 0);
+      }
+    }
+  }
   // FFT facade round trip
   FftPlan fwd(16, 3, Precision::Double, FftDirection::Forward), inv(16, 3, Precision::Double, FftDirection::Inverse);
   auto x = uniform_fill(48, 3);
