@@ -250,6 +250,7 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
 
   // Phases 1-2 (+ reorder to TOSI, cast to cfg[2]) over series [s0, s1).
   auto r2c_series = [&](long s0, long s1) {
+    NvtxRange nr("fftmv:r2c");
     void* xo = static_cast<unsigned char*>(ctx->x.p) + s0 * e2;
     const long cnt = s1 - s0;
     if (payload_prec < 0)
@@ -267,6 +268,7 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
   };
   // Phase 3 SBGEMV in cfg[2] over columns [j0, j1), output cast to cfg[3], TOSI.
   auto gemv_chunk = [&](int c) {
+    NvtxRange nr("fftmv:sbgemv");
     const long j0 = chunk_edge(n, c, C), j1 = chunk_edge(n, c + 1, C);
     const void* A = static_cast<const unsigned char*>(bins) + j0 * lda * (long)e2;
     GemvArgs g;
@@ -294,6 +296,7 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
   };
   // Phases 4-5 (+ reorder back to SOTI, 1/L in cfg[3], unpad, cast cfg[4]) over series [s0, s1).
   auto c2r_series = [&](long s0, long s1) {
+    NvtxRange nr("fftmv:c2r");
     c2r_dispatch(ctx, p[3], p[4], static_cast<unsigned char*>(ctx->y.p) + s0 * e3, n_out, 1, s1 - s0, (int)nt,
                  (int)nt, out + s0 * nt, nt);
   };
@@ -531,6 +534,7 @@ namespace {
 // Returns the payload pointer and its precision. Charged to phase [0]
 // (partition.hpp:204-206).
 std::pair<const void*, int> bcast_payload(fmv_ctx* ctx, void* comm, bool root, const double* in, long n, int p0) {
+  NvtxRange nr("fftmv:broadcast");
   cudaStream_t s = ctx->stream;
   if (p0 == PD) {
     if (!comm) return {in, PD};
@@ -578,6 +582,7 @@ __global__ void k_tree_reduce(T* __restrict__ G, long n, int p, double* __restri
 // (0.8 MB at C2), so gathering p of them costs little. Charged to phase [4]
 // (partition.hpp:178-180). gsize == 1: nothing to do.
 void reduce_partials(fmv_ctx* ctx, void* comm, int gsize, int grank, double* buf, long n, int p4) {
+  NvtxRange nr("fftmv:reduce");
   if (!comm || gsize < 2) {
     // one worker: tree_reduce<float> still casts the lone partial to float and
     // back (2 casts); its value is already float-representable (the unpad
@@ -807,6 +812,7 @@ int fmv_synchronize(fmv_ctx* ctx) {
 
 int fmv_op_create(fmv_ctx* ctx, size_t nm, size_t nd, size_t nt, const double* col, int col_on_device, fmv_op** out) {
   return guarded([&] {
+    NvtxRange nr("fftmv:setup_operator");
     if (!ctx || !out) fail(FMV_EINVAL, "fmv_op_create: null argument");
     if (nm < 1 || nd < 1 || nt < 1) fail(FMV_EINVAL, "ProblemDims: all extents must be >= 1");
     if (!col) fail(FMV_EINVAL, "fmv_op_create: null block column");
@@ -904,6 +910,7 @@ size_t fmv_op_device_bytes(const fmv_op* op) {
 int fmv_matvec_block_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, size_t nrhs, const double* d_in,
                            double* d_out) {
   return guarded([&] {
+    NvtxRange nr(nvtx_matvec_name("matvec_block_async", kind, cfg));
     if (!ctx || !op || !d_in || !d_out) fail(FMV_EINVAL, "fmv_matvec_block_async: null argument");
     check_same_device(ctx, op);
     if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
@@ -916,6 +923,7 @@ int fmv_matvec_block_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char*
 int fmv_matvec_block(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, size_t nrhs, const double* in,
                      double* out, int io_on_device) {
   return guarded([&] {
+    NvtxRange nr(nvtx_matvec_name("matvec_block", kind, cfg));
     if (!ctx || !op || !in || !out) fail(FMV_EINVAL, "fmv_matvec_block: null argument");
     check_same_device(ctx, op);
     if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
@@ -941,6 +949,7 @@ int fmv_matvec_block(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, 
 }
 int fmv_matvec_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* d_in, double* d_out) {
   return guarded([&] {
+    NvtxRange nr(nvtx_matvec_name("matvec_async", kind, cfg));
     if (!ctx || !op || !d_in || !d_out) fail(FMV_EINVAL, "fmv_matvec_async: null argument");
     check_same_device(ctx, op);
     if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
@@ -953,6 +962,7 @@ int fmv_matvec_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, 
 int fmv_matvec(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* in, double* out,
                int io_on_device, fmv_phase_times* times) {
   return guarded([&] {
+    NvtxRange nr(nvtx_matvec_name("matvec", kind, cfg));
     if (!ctx || !op || !in || !out) fail(FMV_EINVAL, "fmv_matvec: null argument");
     if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
     check_same_device(ctx, op);
@@ -965,6 +975,7 @@ int fmv_matvec(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const 
 int fmv_matvec_payload(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, char payload_prec, const void* in,
                        double* out, int io_on_device, fmv_phase_times* times) {
   return guarded([&] {
+    NvtxRange nr(nvtx_matvec_name("matvec_payload", kind, cfg));
     if (!ctx || !op || !in || !out) fail(FMV_EINVAL, "fmv_matvec_payload: null argument");
     if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
     check_same_device(ctx, op);
@@ -1049,6 +1060,7 @@ int fmv_comm_init_2d(fmv_ctx* ctx, int pr, int pc, int rank, const void* id128) 
 int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* in, double* out,
                            int io_on_device, fmv_phase_times* times) {
   return guarded([&] {
+    NvtxRange nr(nvtx_matvec_name("matvec_partitioned", kind, cfg));
     if (!ctx || !op || !out) fail(FMV_EINVAL, "fmv_matvec_partitioned: null argument");
     if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
     check_same_device(ctx, op);
@@ -1107,6 +1119,7 @@ int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* op, int kind, const char*
 int fmv_matvec_partitioned_2d(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* in,
                               double* out, int io_on_device) {
   return guarded([&] {
+    NvtxRange nr(nvtx_matvec_name("matvec_partitioned_2d", kind, cfg));
     if (!ctx || !op || !out) fail(FMV_EINVAL, "fmv_matvec_partitioned_2d: null argument");
     if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
     check_same_device(ctx, op);
@@ -1198,6 +1211,7 @@ int fmv_graph_create(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, 
 }
 
 int fmv_graph_launch(fmv_graph* g) {
+  NvtxRange nr("fftmv:graph_launch");
   return guarded([&] {
     if (!g) fail(FMV_EINVAL, "fmv_graph_launch: null graph");
     DeviceGuard dg(g->device);

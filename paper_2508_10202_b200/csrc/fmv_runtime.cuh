@@ -24,6 +24,7 @@
 
 #include "../../include/fftmv_cuda.h"
 #include "fmv_common.cuh"
+#include <nvtx3/nvToolsExt.h>
 #include "fmv_fft_plan.cuh"
 
 namespace fmv {
@@ -210,6 +211,21 @@ inline int cur_device() {
   int d = 0;
   CK(cudaGetDevice(&d));
   return d;
+}
+
+// NVTX ranges (tracing): one per C-ABI matvec / setup call and one
+// per pipeline phase group (r2c, SBGEMV, c2r, exchange), named "fftmv:...", so
+// an nsys / ncu --nvtx timeline attributes every kernel to the reference's
+// phases. Header-only NVTX3: a pointer test when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  explicit NvtxRange(const std::string& name) { nvtxRangePushA(name.c_str()); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+inline std::string nvtx_matvec_name(const char* what, int kind, const char* cfg) {
+  return std::string("fftmv:") + what + (kind == FMV_FORWARD ? " F " : " F* ") + (cfg ? cfg : "");
 }
 
 // Raise a kernel's dynamic shared-memory cap once per (device, function, size).

@@ -1,0 +1,60 @@
+"""SURVEY.md §5 auxiliary subsystems on the GPU: compute-sanitizer (memcheck,
+synccheck, racecheck) over small matvecs through every kernel family of the hot
+path, and the NVTX ranges the library opens around its calls and phases.
+Run with -m gpu (each sanitizer run takes tens of seconds)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+CASE = os.path.join(ROOT, "tools", "san_case.py")
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+NCU = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+
+
+def _san(tool, args, extra_env=None, timeout=600):
+    env = dict(os.environ, **(extra_env or {}))
+    cmd = [SAN, "--tool", tool, "--error-exitcode", "9", "--target-processes", "all", sys.executable, CASE] + args
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards displayed (0 errors, 0 warnings)" in out, \
+        out[-4000:]
+    return out
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
+def test_sanitizer_clean_small_matvecs(tool):
+    """fp64 / fp32 / fp16-extension SBGEMVs (staged TMA-ring and small-problem
+    kernels), the register FFTs at n_t = 100 and a runtime-plan length, and the
+    block kernels (K = 3)."""
+    out = _san(tool, ["50", "10", "20", "ddddd,dssdd,ddhdd"], {"FMV_SAN_BLOCK": "3"})
+    assert out.count(" ok ") >= 3
+    _san(tool, ["30", "6", "100", "ddddd,sssss"])
+
+
+def test_racecheck_clean_with_arrive_all():
+    """racecheck models the mbarrier release only when every consumer thread
+    arrives (FMV_SBGEMV_ARRIVE_ALL=1)."""
+    _san("racecheck", ["24", "6", "20", "ddddd,dssdd"], {"FMV_SBGEMV_ARRIVE_ALL": "1", "FMV_SAN_BLOCK": "2"})
+
+
+@pytest.mark.parametrize("rng,want,absent", [("fftmv:sbgemv", "k_sbgemv", "k_c2r"), ("fftmv:c2r", "k_c2r", "k_sbgemv"),
+                                              ("fftmv:r2c", "k_r2c", "k_sbgemv")])
+def test_nvtx_ranges_attribute_kernels_to_phases(rng, want, absent):
+    """ncu --nvtx --nvtx-include <phase range>: the kernels launched inside the
+    library's phase range are that phase's and no other."""
+    if not os.path.exists(NCU):
+        pytest.skip("ncu not available")
+    cmd = [NCU, "--nvtx", "--nvtx-include", f"{rng}/", "--metrics", "gpu__time_duration.sum", "--csv",
+           sys.executable, CASE, "20", "4", "20", "ddddd"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
+    assert want in r.stdout, r.stdout[-3000:]
+    assert absent not in r.stdout, r.stdout[-3000:]
