@@ -214,7 +214,7 @@ cudaEvent_t chunk_event(fmv_ctx* ctx, int i) {
 // precision (partition.hpp:198-212); otherwise `in` is double. With `hio`, the
 // host input is copied into `in` chunk by chunk (F) and the output leaves
 // chunk by chunk (F*) on a copy stream, overlapped with the SBGEMV.
-void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5>& p, const void* in,
+void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const Cfg& p, const void* in,
               int payload_prec, double* out, HostIO* hio = nullptr) {
   fmv_op* op = const_cast<fmv_op*>(cop);
   const bool fwd = kind == FMV_FORWARD;
@@ -292,7 +292,7 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
       g.y = static_cast<unsigned char*>(ctx->y.p) + j0 * e3;
       g.sy = n;
     }
-    gemv_run(ctx, p[2], p[3], fwd ? FMV_GEMV_N : FMV_GEMV_C, g);
+    gemv_run(ctx, p[2], p[3], fwd ? FMV_GEMV_N : FMV_GEMV_C, g, p[5] != 0);
   };
   // Phases 4-5 (+ reorder back to SOTI, 1/L in cfg[3], unpad, cast cfg[4]) over series [s0, s1).
   auto c2r_series = [&](long s0, long s1) {
@@ -375,14 +375,14 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5
 
 // Can the block kernel run this (op, cfg)? (fp16 'h' SBGEMV and NoTrans with
 // nd > 256 rows run as K single-RHS pipelines instead.)
-bool block_supported(const fmv_op* op, int kind, const std::array<int, 5>& p) {
-  if (p[2] == PH) return false;
+bool block_supported(const fmv_op* op, int kind, const Cfg& p) {
+  if (p[2] == PH || p[5]) return false;
   return kind != FMV_FORWARD || op->nd <= (size_t)kBlockConsumers;
 }
 
 // run_pipeline over K right-hand sides: in = K SOTI vectors back to back
 // (K*n_in*nt doubles), out likewise; device pointers, enqueued on ctx->stream.
-void pipeline_block(fmv_ctx* ctx, const fmv_op* cop, int kind, const std::array<int, 5>& p, long K, const double* in,
+void pipeline_block(fmv_ctx* ctx, const fmv_op* cop, int kind, const Cfg& p, long K, const double* in,
                     double* out) {
   fmv_op* op = const_cast<fmv_op*>(cop);
   const bool fwd = kind == FMV_FORWARD;
@@ -674,7 +674,7 @@ namespace {
 // `times`, each kernel / copy is bracketed by CUDA events and the
 // PhaseTimings are the per-phase busy times (phases overlap on the host-I/O
 // path, so their sum may exceed total_s, the wall time of the call).
-void matvec_blocking(fmv_ctx* ctx, const fmv_op* op, int kind, const std::array<int, 5>& p, int payload_prec,
+void matvec_blocking(fmv_ctx* ctx, const fmv_op* op, int kind, const Cfg& p, int payload_prec,
                      const void* in, double* out, bool io_on_device, fmv_phase_times* times) {
   const bool fwd = kind == FMV_FORWARD;
   const size_t in_elem = payload_prec < 0 || payload_prec == PD ? 8 : payload_prec == PS ? 4 : 2;

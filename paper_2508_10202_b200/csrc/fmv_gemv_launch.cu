@@ -236,12 +236,6 @@ void run_gemv_o(fmv_ctx* ctx, int p3, int mode, GemvPlan& gp) {
   if (p3 == PD) sbgemv_mode<E, double2>(ctx, mode, gp, false, nullptr);
   else sbgemv_mode<E, float2>(ctx, mode, gp, false, nullptr);
 }
-void run_gemv(fmv_ctx* ctx, const std::array<int, 5>& p, int mode, GemvPlan& gp) {
-  if (p[2] == PD) run_gemv_o<double2>(ctx, p[3], mode, gp);
-  else if (p[2] == PS) run_gemv_o<float2>(ctx, p[3], mode, gp);
-  else run_gemv_o<__half2>(ctx, p[3], mode, gp);
-}
-
 GemvPlan plan_of(const GemvArgs& a) {
   GemvPlan gp = make_gemv(a.A, a.m, a.n, a.batch, a.lda, a.sa, a.x, a.sx, a.y, a.sy);
   gp.p.yacc = a.yacc;
@@ -252,9 +246,10 @@ GemvPlan plan_of(const GemvArgs& a) {
   return gp;
 }
 
-void gemv_run(fmv_ctx* ctx, int p2, int p3, int mode, const GemvArgs& a) {
+void gemv_run(fmv_ctx* ctx, int p2, int p3, int mode, const GemvArgs& a, bool acc64) {
   GemvPlan gp = plan_of(a);
-  if (p2 == PD) run_gemv_o<double2>(ctx, p3, mode, gp);
+  if (acc64 && p2 == PS) run_gemv_o<cf32d>(ctx, p3, mode, gp);  // the 'm' variant
+  else if (p2 == PD) run_gemv_o<double2>(ctx, p3, mode, gp);
   else if (p2 == PS) run_gemv_o<float2>(ctx, p3, mode, gp);
   else run_gemv_o<__half2>(ctx, p3, mode, gp);
 }

@@ -89,17 +89,28 @@ inline int prec_of(char c) {
   }
 }
 
-// config.hpp:36-51 plus the 'h' extension rules.
-inline std::array<int, 5> parse_cfg(const char* cfg) {
+// A parsed config: p[0..4] the five phase precisions (PD / PS / PH), p[5] = 1
+// for the 'm' SBGEMV variant (slot 3 only: fp32 operator and spectrum, fp64
+// accumulation), whose storage precision p[2] is PS.
+using Cfg = std::array<int, 6>;
+
+// config.hpp:36-51 plus the extension rules: 'h' (fp16) at slots 1, 3, 5 and
+// 'm' at slot 3.
+inline Cfg parse_cfg(const char* cfg) {
   if (!cfg) fail(FMV_EINVAL, "precision config is null");
   const size_t len = strnlen(cfg, 16);
   if (len != 5)
     fail(FMV_EINVAL, "precision config must be exactly 5 characters, got " + std::to_string(len));
-  std::array<int, 5> p{};
+  Cfg p{};
   for (int i = 0; i < 5; ++i) {
+    if (cfg[i] == 'm' && i == 2) {
+      p[i] = PS;
+      p[5] = 1;
+      continue;
+    }
     if (cfg[i] != 'd' && cfg[i] != 's' && cfg[i] != 'h')
       fail(FMV_EINVAL, std::string("precision config: invalid character '") + cfg[i] + "' at position " +
-                           std::to_string(i + 1) + " (expected 'd', 's' or 'h')");
+                           std::to_string(i + 1) + " (expected 'd', 's' or 'h'; 'm' at position 3)");
     p[i] = prec_of(cfg[i]);
   }
   if (p[1] == PH || p[3] == PH)
@@ -107,8 +118,9 @@ inline std::array<int, 5> parse_cfg(const char* cfg) {
   return p;
 }
 
-// Logical cast passes of run_pipeline (matvec.hpp:88, :121-125, :163, :189-190).
-inline uint64_t count_casts(const std::array<int, 5>& p, bool payload) {
+// Logical cast passes of run_pipeline (matvec.hpp:88, :121-125, :163, :189-190);
+// 'm' rounds exactly where 's' does.
+inline uint64_t count_casts(const Cfg& p, bool payload) {
   uint64_t n = 0;
   if (!payload && p[0] != PD) ++n;
   if (p[0] != p[1]) ++n;
@@ -547,7 +559,8 @@ struct GemvArgs {
   int K = 1;             // block SBGEMV: right-hand sides, per-RHS strides of x / y within a bin
   long sxr = 0, syr = 0;
 };
-void gemv_run(fmv_ctx* ctx, int p2, int p3, int mode, const GemvArgs& a);
+// acc64: the 'm' variant (p2 == PS storage, fp64 accumulators)
+void gemv_run(fmv_ctx* ctx, int p2, int p3, int mode, const GemvArgs& a, bool acc64 = false);
 // Block (multi-RHS) SBGEMV; false when the shape is outside the kernel's limits.
 bool block_gemv_run(fmv_ctx* ctx, int p2, int p3, int mode, const GemvArgs& a);
 constexpr int kBlockMax = 8;

@@ -59,15 +59,18 @@ class ProblemDims:
 
 # ------------------------------------------------------------- precision ---
 class Precision(enum.IntEnum):
-    """precision.hpp:15; Half is this project's fp16 extension (appended so
-    Single=0 / Double=1 keep their values)."""
+    """precision.hpp:15; Half is this project's fp16 extension and
+    SingleAccDouble ('m', SBGEMV slot only) its fp32-storage / fp64-accumulate
+    SBGEMV variant, appended so Single=0 / Double=1 keep
+    their values."""
 
     Single = 0
     Double = 1
     Half = 2
+    SingleAccDouble = 3
 
 
-_P2C = {Precision.Double: "d", Precision.Single: "s", Precision.Half: "h"}
+_P2C = {Precision.Double: "d", Precision.Single: "s", Precision.Half: "h", Precision.SingleAccDouble: "m"}
 _C2P = {v: k for k, v in _P2C.items()}
 
 
@@ -96,15 +99,16 @@ class PrecisionConfig:
 
 
 def parse_precision_config(s: str, allow_half: bool = True) -> PrecisionConfig:
-    """config.hpp:36-51 (errors name the 1-based position); 'h' accepted at
-    positions 1, 3, 5 as the fp16 extension."""
+    """config.hpp:36-51 (errors name the 1-based position); the extensions
+    (allow_half): 'h' (fp16) at positions 1, 3, 5 and 'm' (fp32 storage, fp64
+    accumulation) at position 3."""
     if len(s) != 5:
         raise ValueError(f"precision config must be exactly 5 characters, got {len(s)}")
     out = []
     for i, ch in enumerate(s):
-        ok = ch in ("d", "s") or (allow_half and ch == "h" and i in (0, 2, 4))
+        ok = ch in ("d", "s") or (allow_half and ((ch == "h" and i in (0, 2, 4)) or (ch == "m" and i == 2)))
         if not ok:
-            exp = "'d' or 's'" + (" (or 'h' at positions 1, 3, 5)" if allow_half else "")
+            exp = "'d' or 's'" + (" (or 'h' at positions 1, 3, 5, 'm' at position 3)" if allow_half else "")
             raise ValueError(f"precision config: invalid character '{ch}' at position {i + 1} (expected {exp})")
         out.append(_C2P[ch])
     return PrecisionConfig(tuple(out))
@@ -112,8 +116,8 @@ def parse_precision_config(s: str, allow_half: bool = True) -> PrecisionConfig:
 
 def enumerate_configs(include_half: bool = False) -> list:
     """config.hpp:55-65: the 32 {d,s} configs in lexicographic order ('d' < 's').
-    include_half=True appends the 'h' variants (fp16 at phases 1/3/5), ordered
-    the same way, after the 32 reference configs."""
+    include_half=True appends the extension variants ('h' at phases 1/3/5,
+    'm' at phase 3), ordered the same way, after the 32 reference configs."""
     allc = []
     for bits in range(32):
         allc.append(PrecisionConfig(tuple(Precision.Single if (bits >> (4 - i)) & 1 else Precision.Double
@@ -122,7 +126,7 @@ def enumerate_configs(include_half: bool = False) -> list:
         seen = {c.render() for c in allc}
         import itertools
 
-        for combo in itertools.product("dsh", "ds", "dsh", "ds", "dsh"):
+        for combo in itertools.product("dsh", "ds", "dshm", "ds", "dsh"):
             s = "".join(combo)
             if s not in seen:
                 allc.append(parse_precision_config(s))

@@ -47,6 +47,9 @@ static void host_checks() {
   EXPECT(ProblemDims(5, 3, 7).fft_len() == 14 && ProblemDims(5, 3, 7).n_bins() == 8);
   EXPECT(parse_precision_config("dssdd").render() == "dssdd");
   EXPECT(throws_invalid([] { parse_precision_config("dsxdd"); }));
+  EXPECT(parse_precision_config("ddmdd").render() == "ddmdd");  // fp32 storage, fp64 accumulation (slot 3 only)
+  EXPECT(parse_precision_config("ddmdd")[2] == Precision::SingleAccDouble);
+  EXPECT(throws_invalid([] { parse_precision_config("dmddd"); }));
   EXPECT(throws_invalid([] { parse_precision_config("dss"); }));
   auto all = enumerate_configs();
   EXPECT(all.size() == 32 && all.front().render() == "ddddd" && all.back().render() == "sssss");

@@ -97,7 +97,16 @@ def test_precision_config_grammar():
     assert allc[0] == "ddddd" and allc[-1] == "sssss"
     assert all(F.parse_precision_config(s).render() == s for s in allc)
     ext = [c.render() for c in F.enumerate_configs(include_half=True)]
-    assert ext[:32] == allc and "ddhdd" in ext and "hdhdh" in ext and len(ext) == 3 * 2 * 3 * 2 * 3
+    assert ext[:32] == allc and "ddhdd" in ext and "hdhdh" in ext and len(ext) == 3 * 2 * 4 * 2 * 3
+    # 'm' (fp32 storage, fp64 accumulation) exists at the SBGEMV slot only
+    assert "ddmdd" in ext and "sdmsh" in ext and not any("m" in c[:2] + c[3:] for c in ext)
+    c = F.parse_precision_config("ddmdd")
+    assert c[2] == F.Precision.SingleAccDouble and c.render() == "ddmdd"
+    for bad, pos in (("mdddd", 1), ("dmddd", 2), ("dddmd", 4), ("ddddm", 5)):
+        with pytest.raises(ValueError, match=f"position {pos}"):
+            F.parse_precision_config(bad)
+    with pytest.raises(ValueError, match="position 3"):
+        F.parse_precision_config("ddmdd", allow_half=False)
 
 
 def test_dims_and_block_vectors():

@@ -66,3 +66,18 @@ def test_c3_half_extension(c3):
         ef = rel(F.forward_matvec(op, m, cfg, timings=False).output.data, base[0])
         ea = rel(F.adjoint_matvec(op, d, cfg, timings=False).output.data, base[1])
         assert 0 < ef <= HALF_TOL and 0 < ea <= HALF_TOL, (cfg, ef, ea)
+
+
+def test_c3_fp64_accumulate_variant(c3):
+    """The 'm' SBGEMV variant (fp32 operator and spectrum, fp64 accumulation;
+    SURVEY.md App. A4): at C2 its error is the input-rounding floor, below the
+    fp32-accumulating 's' config and below tau = 1e-7, for F and F*."""
+    op, m, d, ref_out = c3
+    base = {0: ref_out[(0, "ddddd")], 1: ref_out[(1, "ddddd")]}
+    for kind, x, fn in ((0, m, F.forward_matvec), (1, d, F.adjoint_matvec)):
+        em = rel(fn(op, x, "ddmdd", timings=False).output.data, base[kind])
+        es = rel(fn(op, x, "ddsdd", timings=False).output.data, base[kind])
+        assert 0 < em < 1e-7 and em < es, (kind, em, es)
+        for cfg in ("dsmdd", "ssmss", "ddmds"):
+            e = rel(fn(op, x, cfg, timings=False).output.data, base[kind])
+            assert e <= 2 * rel(ref_out[(kind, cfg.replace("m", "s"))], base[kind]), (kind, cfg, e)
