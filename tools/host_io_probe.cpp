@@ -52,6 +52,36 @@ int main() {
   std::printf(", \"h2d_pinned_GBs\": %.1f", dma(dev, pin, cudaMemcpyHostToDevice));
   std::printf(", \"d2h_pinned_GBs\": %.1f", dma(pin, dev, cudaMemcpyDeviceToHost));
   std::printf(", \"h2d_pageable_GBs\": %.1f", dma(dev, src.data(), cudaMemcpyHostToDevice));
+  {  // pinned H2D split over k streams (copy engines) at once
+    cudaStream_t st[4];
+    for (auto& x : st) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+    for (int k : {1, 2, 4}) {
+      const int R = 10;
+      const size_t part = bytes / k;
+      cudaDeviceSynchronize();
+      const double t0 = now();
+      for (int r = 0; r < R; ++r)
+        for (int i = 0; i < k; ++i)
+          cudaMemcpyAsync((char*)dev + i * part, (char*)pin + i * part, part, cudaMemcpyHostToDevice, st[i]);
+      cudaDeviceSynchronize();
+      std::printf(", \"h2d_pinned_%dstreams_GBs\": %.1f", k, bytes * R / (now() - t0) / 1e9);
+      const double t1 = now();
+      for (int r = 0; r < R; ++r)
+        for (int i = 0; i < k; ++i)
+          cudaMemcpyAsync((char*)pin + i * part, (char*)dev + i * part, part, cudaMemcpyDeviceToHost, st[i]);
+      cudaDeviceSynchronize();
+      std::printf(", \"d2h_pinned_%dstreams_GBs\": %.1f", k, bytes * R / (now() - t1) / 1e9);
+    }
+    // H2D and D2H at the same time (F's input while F*'s output drains)
+    const int R = 10;
+    const double t2 = now();
+    for (int r = 0; r < R; ++r) {
+      cudaMemcpyAsync(dev, pin, bytes / 2, cudaMemcpyHostToDevice, st[0]);
+      cudaMemcpyAsync((char*)pin + bytes / 2, (char*)dev + bytes / 2, bytes / 2, cudaMemcpyDeviceToHost, st[1]);
+    }
+    cudaDeviceSynchronize();
+    std::printf(", \"h2d_plus_d2h_concurrent_GBs_total\": %.1f", bytes * R / (now() - t2) / 1e9);
+  }
   std::printf(", \"d2h_pageable_GBs\": %.1f", dma(dst.data(), dev, cudaMemcpyDeviceToHost));
   {  // a 40 MB pinned H2D in flight while T threads copy 40 MB pageable -> pinned
     double* pin2 = nullptr;
