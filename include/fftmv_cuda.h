@@ -13,7 +13,8 @@
  *                                                                (matvec.hpp:291-299)
  *   - cfg: 5 chars, positions = phases {pad/broadcast, fft, sbgemv, ifft,
  *     unpad/reduce} (config.hpp:14-33), chars 'd' or 's', plus the 'h' (fp16)
- *     extension at positions 0, 2 and 4.
+ *     extension at positions 0, 2 and 4 and the 'm' extension at position 2
+ *     (SBGEMV on the fp32 operator and spectrum with fp64 accumulation).
  * Return codes: FMV_OK, or an error code with a message in fmv_last_error()
  * (thread-local). The C++ wrapper maps FMV_EINVAL to std::invalid_argument
  * and everything else to std::runtime_error, like the reference.
@@ -116,7 +117,7 @@ int fmv_matvec_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, 
  * fmv_matvec; the per-bin SBGEMV handles up to 8 (FORWARD) / 4 (ADJOINT) RHS
  * per operator pass (the operator is read from HBM once per pass instead of
  * once per RHS). Per-RHS results equal fmv_matvec's up to summation order
- * (fp64: ~1e-15 relative). 'h' SBGEMV configs and FORWARD with nd > 416 run
+ * (fp64: ~1e-15 relative). 'h' and 'm' SBGEMV configs and FORWARD with nd > 416 run
  * as nrhs single-RHS pipelines. Blocking; host pointers unless io_on_device. */
 int fmv_matvec_block(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, size_t nrhs, const double* in,
                      double* out, int io_on_device);
