@@ -334,6 +334,39 @@ bool sbgemm_block_t(fmv_ctx* ctx, GemvPlan& gp) {
       }
     }
   }
+  if constexpr (MODE != GM_N && std::is_same<E, double2>::value) {
+    // two-columns-per-lane ConjTrans variant: W warps x 4 column groups x 2
+    // columns per round, stages of exactly that many columns
+    const int W = env_int("FMV_BLOCK_C2_WARPS", 8);  // tools/bench_block.py: W = 4..8 -> K=4 1.90 / 2.12 / 1.76 / 1.46 / 1.35 ms
+    if (!wide && (K == 4 || K == 2) && K == KR && W >= 2 && W * 32 <= kBlockConsumers && env_int("FMV_BLOCK_C2", 1)) {
+      GemvParams& q = gp.p;
+      auto up128 = [](long v) { return (int)((v + 127) / 128 * 128); };
+      const long es = (long)sizeof(E);
+      const int Jc = W * 8;
+      const long max_a = ((long)(Jc - 1) * q.lda + q.m) * es;
+      const int a_slot = up128(max_a + 32), xr_slot = up128((long)q.m * es + 32);
+      const long xs = (long)KR * xr_slot;
+      int nst = 3;
+      auto smem_of = [&](int ns, bool xres) {
+        return (size_t)512 + (size_t)ns * (a_slot + (xres ? 0 : xs)) + (xres ? 2 * xs : 0);
+      };
+      if (smem_of(3, true) > 227 * 1024) nst = 2;
+      const bool xres = (q.n + Jc - 1) / Jc >= nst;
+      if (max_a <= 120 * 1024 && smem_of(nst, xres) <= 227 * 1024) {
+        q.Jc = Jc;
+        q.a_slot = a_slot;
+        q.xr_slot = xr_slot;
+        q.nstage = nst;
+        q.xres = xres;
+        q.xres_slot = 0;
+        gp.smem = smem_of(nst, xres);
+        gp.block = W * 32 + 32;
+        if (K == 4) sbgemm_block_launch_t<MODE, E, O, 4, L1, 4>(ctx, gp);
+        else sbgemm_block_launch_t<MODE, E, O, 2, L1, 2>(ctx, gp);
+        return true;
+      }
+    }
+  }
   if (KR == 2) wide ? sbgemm_block_launch_t<MODE, E, O, 2, L2>(ctx, gp) : sbgemm_block_launch_t<MODE, E, O, 2, L1>(ctx, gp);
   else if (KR == 4) wide ? sbgemm_block_launch_t<MODE, E, O, 4, L2>(ctx, gp) : sbgemm_block_launch_t<MODE, E, O, 4, L1>(ctx, gp);
   else wide ? sbgemm_block_launch_t<MODE, E, O, 8, L2>(ctx, gp) : sbgemm_block_launch_t<MODE, E, O, 8, L1>(ctx, gp);

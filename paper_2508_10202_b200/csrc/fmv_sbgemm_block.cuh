@@ -36,11 +36,12 @@ namespace fmv {
 #ifndef FMV_BLOCK_MINB
 #define FMV_BLOCK_MINB 1  // resident CTAs per SM
 #endif
-// KX > 0 (NoTrans fp64 only): exactly KX = KR right-hand sides and x slices
-// XR bytes apart in shared memory, both compile-time -- the column loop then
-// has no per-RHS predicates and every x read is one LDS.128 at an immediate
-// offset from a single per-column base (the runtime-K loop spent ~30
-// integer / predicate instructions per 32 DFMAs on this).
+// KX > 0, NoTrans fp64: exactly KX = KR right-hand sides and x slices XR
+// bytes apart in shared memory, both compile-time -- the column loop then has
+// no per-RHS predicates and every x read is one LDS.128 at an immediate offset
+// from a single per-column base (the runtime-K loop spent ~30 integer /
+// predicate instructions per 32 DFMAs on this).
+// KX > 0, ConjTrans: exactly KX right-hand sides, two columns per lane.
 template <int MODE, class E, class O, int KR, int LPC, int KX = 0, int XR = 0>
 __global__ void __launch_bounds__(FMV_BLOCK_CONS + 32, FMV_BLOCK_MINB) k_sbgemm_block(const GemvParams p) {
   using Tr = ET<E>;
@@ -262,6 +263,74 @@ __global__ void __launch_bounds__(FMV_BLOCK_CONS + 32, FMV_BLOCK_MINB) k_sbgemm_
         }
         bar_consumers(ncons);
       }
+    }
+  } else if constexpr (KX > 0) {
+    // ConjTrans, exactly KX right-hand sides, TWO columns per lane: lane
+    // (sub, li) takes rows li, li+LPC, ... of columns jb+sub and jb+CPW+sub,
+    // so every D_b[i, k] read from shared memory serves two columns. A 128-bit
+    // shared load costs four quarter-warp wavefronts whatever its broadcast,
+    // and the K x reads were 80 % of the one-column kernel's LSU wavefronts
+    // (DESIGN.md §9.1); the host gives this variant fewer consumer warps and
+    // stages of 8 columns per warp so every warp has its two columns.
+    static_assert(KX == KR, "exact-K variant");
+    constexpr int CPW = 32 / LPC;
+    const int W = ncons / 32;
+    const int w = t >> 5;
+    const int sub = lane / LPC;
+    const int li = lane - sub * LPC;
+    for (SegIter sg(c0, c1, p); sg.more(); sg.advance(p)) {
+      sg.load(p);
+      const int s = sg.s;
+      const unsigned char* a0 = p.A + (sg.b * p.sa + sg.j * p.lda) * es;
+      const unsigned char* base = stages + (long)s * slot;
+      const E* As = reinterpret_cast<const E*>(base + (reinterpret_cast<uintptr_t>(a0) & 15));
+      const unsigned char* xb = p.xres ? xres_base + (sg.b & 1) * (long)xs_bytes : base + p.a_slot;
+      const E* Xs[KX];
+#pragma unroll
+      for (int k = 0; k < KX; ++k) {
+        const unsigned char* x0 = p.x + (sg.b * p.sx + (long)k * p.sxr) * es;
+        Xs[k] = reinterpret_cast<const E*>(xb + k * p.xr_slot + (reinterpret_cast<uintptr_t>(x0) & 15));
+      }
+      O* yb = reinterpret_cast<O*>(p.y) + sg.b * p.sy + sg.j;
+      mbar_wait_sleep(&full[s], sg.par);
+      const int cnt = (int)sg.cnt;
+      for (int jb = w * 2 * CPW; jb < cnt; jb += W * 2 * CPW) {
+        const int ja = jb + sub, jc = jb + CPW + sub;
+        const bool va = ja < cnt, vc = jc < cnt;
+        Acc acca[KX], accc[KX];
+#pragma unroll
+        for (int k = 0; k < KX; ++k) acca[k] = accc[k] = Tr::zero();
+        if (va) {
+          const E* cola = As + (long)ja * p.lda;
+          const E* colc = As + (long)(vc ? jc : ja) * p.lda;  // (a valid column when jc is past the stage)
+          for (int i = li; i < p.m; i += LPC) {
+            const E a = cola[i], c = colc[i];
+#pragma unroll
+            for (int k = 0; k < KX; ++k) {
+              const E x = Xs[k][i];
+              acca[k] = Tr::macc(acca[k], a, x);
+              accc[k] = Tr::macc(accc[k], c, x);
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < KX; ++k) {
+#pragma unroll
+          for (int o = LPC >> 1; o > 0; o >>= 1) {
+            acca[k] = Tr::add(acca[k], Tr::shfl_xor(acca[k], o));
+            accc[k] = Tr::add(accc[k], Tr::shfl_xor(accc[k], o));
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < KX; ++k) {
+          if (k % LPC == li) {
+            if (va) yb[(long)k * p.syr + ja] = out_cast<O>(acca[k]);
+            if (vc) yb[(long)k * p.syr + jc] = out_cast<O>(accc[k]);
+          }
+        }
+      }
+      __syncwarp();
+      if (p.arrive_all || lane == 0) mbar_arrive(&empty[s]);
     }
   } else {
     // LPC lanes per column split its m rows (lane li: rows li, li+LPC, ...);
