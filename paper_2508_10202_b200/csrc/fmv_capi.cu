@@ -823,19 +823,29 @@ int fmv_op_create(fmv_ctx* ctx, size_t nm, size_t nd, size_t nt, const double* c
     op->nd = nd;
     op->nt = nt;
     const size_t S = nd * nm, nb = nt + 1;
-    CK(cudaMalloc(&op->bins_d, nb * S * sizeof(double2) + 256));
+    // device allocations are released on every error path (an out-of-memory
+    // operator returns FMV_ENOMEM and leaves the context usable)
+    struct Guard {
+      void* bins = nullptr;
+      void* tmp = nullptr;
+      ~Guard() {
+        if (tmp) cudaFree(tmp);
+        if (bins) cudaFree(bins);
+      }
+    } g;
+    CK(cudaMalloc(&g.bins, nb * S * sizeof(double2) + 256));
+    op->bins_d = g.bins;
     const double* dcol = col;
-    void* tmp = nullptr;
     if (!col_on_device) {
-      CK(cudaMalloc(&tmp, nt * S * sizeof(double)));
-      CK(cudaMemcpyAsync(tmp, col, nt * S * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-      dcol = static_cast<const double*>(tmp);
+      CK(cudaMalloc(&g.tmp, nt * S * sizeof(double)));
+      CK(cudaMemcpyAsync(g.tmp, col, nt * S * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      dcol = static_cast<const double*>(g.tmp);
     }
     // operator.hpp:99-125: every (i,j) series, time-outer in the column,
     // padded to 2nt and r2c'd in fp64, written bin-major.
     r2c_dispatch<double>(ctx, PD, PD, PD, dcol, 1, (long)S, (long)S, (int)nt, (int)nt, op->bins_d, (long)S, 1);
     CK(cudaStreamSynchronize(ctx->stream));
-    if (tmp) cudaFree(tmp);
+    g.bins = nullptr;  // owned by the operator from here on
     *out = op.release();
   });
 }
