@@ -245,10 +245,10 @@ def run_ours(args, rank, world, local_rank):
                                            ctypes.c_void_p(dout.data_ptr())))
             _capi.check(L.fmv_matvec_async(ctx.handle, op.handle, 1, cb, ctypes.c_void_p(d.data_ptr()),
                                            ctypes.c_void_p(mout.data_ptr())))
-        else:
+        else:  # enqueued like the single-GPU path; ctx.synchronize() waits under the NCCL watch
             for kind, x, y in ((0, m, dout), (1, d, mout)):
-                _capi.check(L.fmv_matvec_partitioned(ctx.handle, op.handle, kind, cb, ctypes.c_void_p(x.data_ptr()),
-                                                     ctypes.c_void_p(y.data_ptr()), 1, None))
+                _capi.check(L.fmv_matvec_partitioned_async(ctx.handle, op.handle, kind, cb,
+                                                           ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr())))
 
     def barrier():
         if dist is not None:
@@ -480,6 +480,12 @@ def main():
         args.warmup = 3
     if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
         relaunch_under_torchrun(args)  # does not return
+    # stdout carries exactly one JSON line: keep the real stdout for it and send
+    # everything else written to fd 1 (NCCL's version banner, library prints)
+    # to stderr
+    json_out = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
     local_rank = env_int("LOCAL_RANK", 0)
@@ -502,7 +508,7 @@ def main():
     else:
         line = run_ours(args, rank, world, local_rank)
     if rank == 0 and line is not None:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=json_out, flush=True)
     if world > 1 and args.impl == "ours":
         import torch.distributed as dist
 

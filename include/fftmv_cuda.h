@@ -79,6 +79,8 @@ uint64_t fmv_ctx_launches(fmv_ctx* ctx);
 int fmv_ctx_set_profiling(fmv_ctx* ctx, int enable);
 /* kernel classes: 0 r2c, 1 sbgemv-N, 2 sbgemv-C, 3 c2r, 4 other */
 int fmv_ctx_profile_read(fmv_ctx* ctx, double* ms_per_class5, uint64_t* launches_per_class5, int reset);
+/* Waits for the ctx stream; with communicators, under the NCCL error / timeout
+ * watch of the partitioned entry points. */
 int fmv_synchronize(fmv_ctx* ctx);
 
 /* ---- operator: setup_operator (operator.hpp:99-125) ---- */
@@ -184,6 +186,12 @@ int fmv_comm_size(const fmv_ctx* ctx, int* nranks, int* rank);
  *   precision; out = this rank's m slice (partition.hpp:187-217). */
 int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* shard, int kind, const char* cfg, const double* in,
                            double* out, int io_on_device, fmv_phase_times* times);
+/* Non-blocking fmv_matvec_partitioned: device pointers, the shard pipeline and
+ * the collectives enqueued on the ctx stream, no host wait -- consecutive
+ * partitioned matvecs pipeline like fmv_matvec_async. fmv_synchronize(ctx)
+ * waits with the same NCCL error / timeout watch. */
+int fmv_matvec_partitioned_async(fmv_ctx* ctx, const fmv_op* shard, int kind, const char* cfg, const double* d_in,
+                                 double* d_out);
 
 /* ---- 2-D pr x pc grid ----
  * rank = ri*pc + cj. Splits the world communicator into a row communicator

@@ -71,6 +71,7 @@ def lib() -> ctypes.CDLL:
         "fmv_comm_size": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int)]),
         "fmv_matvec_partitioned": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_void_p, c_void_p, c_int,
                                            POINTER(PhaseTimesC)]),
+        "fmv_matvec_partitioned_async": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_void_p, c_void_p]),
         "fmv_graph_create": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_void_p, c_void_p, POINTER(c_void_p)]),
         "fmv_graph_launch": (c_int, [c_void_p]),
         "fmv_graph_destroy": (c_int, [c_void_p]),

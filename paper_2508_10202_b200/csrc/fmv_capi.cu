@@ -710,6 +710,21 @@ void matvec_blocking(fmv_ctx* ctx, const fmv_op* op, int kind, const Cfg& p, int
   CK(cudaStreamSynchronize(s));
   if (times) collect_phase_times(ctx, ctx->te[0], ctx->te[1], times);
 }
+// partition.hpp:157-217 on this rank's shard, enqueued on ctx->stream:
+// F: the shard pipeline on the local m slice, then the cfg[4] fixed-tree sum
+// of the partial d over the communicator; F*: rank 0's d cast to cfg[0] and
+// broadcast, then the shard pipeline from the payload.
+void partitioned_enqueue(fmv_ctx* ctx, const fmv_op* op, int kind, const Cfg& p, const double* din, double* dout,
+                         HostIO* hp) {
+  const size_t nt = op->nt;
+  if (kind == FMV_FORWARD) {
+    pipeline(ctx, op, kind, p, din, -1, dout, hp);
+    reduce_partials(ctx, ctx->comm, ctx->nranks, ctx->rank, dout, (long)(op->nd * nt), p[4]);
+  } else {
+    const auto pay = bcast_payload(ctx, ctx->comm, ctx->rank == 0, din, (long)(op->nd * nt), p[0]);
+    pipeline(ctx, op, kind, p, pay.first, p[0] == PD && !ctx->comm ? -1 : pay.second, dout, hp);
+  }
+}
 }  // namespace
 
 extern "C" {
@@ -806,7 +821,7 @@ int fmv_synchronize(fmv_ctx* ctx) {
   return guarded([&] {
     if (!ctx) fail(FMV_EINVAL, "null ctx");
     DeviceGuard dg(ctx->device);
-    CK(cudaStreamSynchronize(ctx->stream));
+    comm_sync(ctx);  // a plain stream sync without communicators
   });
 }
 
@@ -1099,19 +1114,25 @@ int fmv_matvec_partitioned(fmv_ctx* ctx, const fmv_op* op, int kind, const char*
       dout = static_cast<double*>(ctx->io_out.p);
     }
     HostIO* hp = io_on_device ? nullptr : &hio;
-    if (fwd) {
-      // partition.hpp:157-182: full-length partial d per rank, summed in cfg[4].
-      pipeline(ctx, op, kind, p, din, -1, dout, hp);
-      reduce_partials(ctx, ctx->comm, ctx->nranks, ctx->rank, dout, (long)(op->nd * nt), p[4]);
-      if (!io_on_device) copy_async(ctx, 4, out, dout, n_out * sizeof(double), cudaMemcpyDeviceToHost, s);
-    } else {
-      // partition.hpp:187-217: cast d to cfg[0] once, broadcast, pad from payload.
-      const auto pay = bcast_payload(ctx, ctx->comm, ctx->rank == 0, din, (long)(op->nd * nt), p[0]);
-      pipeline(ctx, op, kind, p, pay.first, p[0] == PD && !ctx->comm ? -1 : pay.second, dout, hp);
-    }
+    partitioned_enqueue(ctx, op, kind, p, din, dout, hp);
+    if (fwd && !io_on_device) copy_async(ctx, 4, out, dout, n_out * sizeof(double), cudaMemcpyDeviceToHost, s);
     if (times) CK(cudaEventRecord(ctx->te[1], s));
     comm_sync(ctx);
     if (times) collect_phase_times(ctx, ctx->te[0], ctx->te[1], times);
+  });
+}
+
+int fmv_matvec_partitioned_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* d_in,
+                                 double* d_out) {
+  return guarded([&] {
+    NvtxRange nr(nvtx_matvec_name("matvec_partitioned_async", kind, cfg));
+    if (!ctx || !op || !d_out) fail(FMV_EINVAL, "fmv_matvec_partitioned_async: null argument");
+    if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
+    check_same_device(ctx, op);
+    if ((kind == FMV_FORWARD || ctx->rank == 0) && !d_in) fail(FMV_EINVAL, "fmv_matvec_partitioned_async: null input");
+    const auto p = parse_cfg(cfg);
+    DeviceGuard dg(ctx->device);
+    partitioned_enqueue(ctx, op, kind, p, d_in, d_out, nullptr);
   });
 }
 

@@ -6,6 +6,7 @@ host-staged NCCL test transport, so every rank can use cuda:0. torch.distributed
 inside libfftmv_cuda (fmv_matvec_partitioned / fmv_matvec_partitioned_2d).
 Writes this rank's outputs to <outdir>/rank<r>.npz.
 """
+import ctypes
 import os
 import sys
 
@@ -18,6 +19,7 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import paper_2508_10202_b200 as F  # noqa: E402
+from paper_2508_10202_b200 import _capi  # noqa: E402
 from conftest import make_inputs  # noqa: E402
 
 CFGS = ("ddddd", "dddds", "sdddd", "sssss", "hdddh")
@@ -44,6 +46,19 @@ def main():
             # device-resident I/O through the same entry point
             res[f"Fdev_{cfg}"] = dm.forward(torch.from_numpy(m[lo * nt:hi * nt]).cuda(), cfg).cpu().numpy()
             res[f"Adev_{cfg}"] = dm.adjoint(torch.from_numpy(d).cuda(), cfg).cpu().numpy()
+            # the async entry: F and F* enqueued back to back (two collectives in
+            # flight on the stream), one fmv_synchronize for both
+            xf = torch.from_numpy(m[lo * nt:hi * nt]).cuda()
+            xa = torch.from_numpy(d).cuda()
+            yf = torch.empty(nd * nt, dtype=torch.float64, device="cuda")
+            ya = torch.empty((hi - lo) * nt, dtype=torch.float64, device="cuda")
+            torch.cuda.synchronize()
+            L = _capi.lib()
+            for kind, x, y in ((0, xf, yf), (1, xa, ya)):
+                _capi.check(L.fmv_matvec_partitioned_async(ctx.handle, shard.handle, kind, cfg.encode(),
+                                                           ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr())))
+            ctx.synchronize()
+            res[f"Fasync_{cfg}"], res[f"Aasync_{cfg}"] = yf.cpu().numpy(), ya.cpu().numpy()
         out, t = dm.forward(m[lo * nt:hi * nt], "ddddd", times=True)
         res["F_times"] = np.array(list(t.phase_s) + [t.total_s])
         res["lohi"] = np.array([lo, hi])
