@@ -103,6 +103,7 @@ def exported_symbols() -> list[str]:
         "fmv_uniform_fill", "fmv_non_representable_fill", "fmv_relative_error", "fmv_fft_r2c", "fmv_fft_c2r",
         "fmv_matvec_block", "fmv_matvec_block_async", "fmv_comm_init_2d", "fmv_matvec_partitioned_2d",
         "fmv_graph_create", "fmv_graph_launch", "fmv_graph_destroy", "fmv_matvec_payload", "fmv_comm_size",
+        "fmv_matvec_partitioned_async", "fmv_host_copy",
     ]
 
 
