@@ -67,5 +67,30 @@ for _ in range(a.reps):
     fwd()
     adj()
 ms, n = ctx.profile_read(reset=True)
+# host I/O (pinned buffers, blocking fmv_matvec): wall time per call
+import time
+mp, dp = m.cpu().pin_memory(), d.cpu().pin_memory()
+yp, mpo = torch.empty(ND * NT, dtype=torch.float64).pin_memory(), torch.empty(NM * NT, dtype=torch.float64).pin_memory()
+
+
+def hf():
+    _capi.check(L.fmv_matvec(ctx.handle, op.handle, 0, cb, ctypes.c_void_p(mp.data_ptr()), ctypes.c_void_p(yp.data_ptr()), 0, None))
+
+
+def ha():
+    _capi.check(L.fmv_matvec(ctx.handle, op.handle, 1, cb, ctypes.c_void_p(dp.data_ptr()), ctypes.c_void_p(mpo.data_ptr()), 0, None))
+
+
+def wall(fn):
+    for _ in range(3):
+        fn()
+    t0 = time.perf_counter()
+    for _ in range(a.reps):
+        fn()
+    return (time.perf_counter() - t0) * 1e3 / a.reps
+
+
+host = {"ms_F": wall(hf), "ms_Fstar": wall(ha), "ms_step": wall(lambda: (hf(), ha()))}
+print(json.dumps({"host_pinned": host}))
 print(json.dumps({"env": {k: v for k, v in os.environ.items() if k.startswith("FMV_")}, "cfg": a.cfg, "ms_F": tf, "ms_Fstar": ta,
                   "ms_step": ts, "class_ms_per_step": [x / a.reps for x in ms], "class_launches_per_step": [x / a.reps for x in n]}))
