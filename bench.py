@@ -204,20 +204,20 @@ def workload_config(world, cfg):
 
 
 # ------------------------------------------------------------------- ours ---
-def run_ours(args, rank, world, local_rank):
+def run_ours(args, rank, world, device):
     import torch
 
     import paper_2508_10202_b200 as F
     from paper_2508_10202_b200 import _capi
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    dev = torch.device("cuda", device)
     dist = None
     if world > 1:
         import torch.distributed as dist  # noqa: F811
 
     col, m_h, d_h = make_inputs(rank)
-    ctx = F.Context(local_rank)
+    ctx = F.Context(device)
     op = F.setup_operator(F.BlockColumn(F.ProblemDims(NM, ND, NT), col), ctx)
     cfg = args.cfg
     if cfg[2] == "s":
@@ -275,7 +275,7 @@ def run_ours(args, rank, world, local_rank):
         return ms
 
     # ---- device-resident throughput (value) + per-kernel CUDA events
-    clk = ClockSampler(local_rank).__enter__()  # samples through warm-up, timed and e2e regions
+    clk = ClockSampler(device).__enter__()  # samples through warm-up, timed and e2e regions
     for _ in range(args.warmup):
         step_device()
     ctx.synchronize()
@@ -447,7 +447,7 @@ def relaunch_under_torchrun(args):
     import torch
 
     n = torch.cuda.device_count()
-    if n < args.gpus:
+    if n < args.gpus and os.environ.get("FMV_BENCH_SHARED_GPU") != "1":
         raise SystemExit(f"bench: --gpus {args.gpus} but only {n} visible GPUs")
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -489,24 +489,32 @@ def main():
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
     local_rank = env_int("LOCAL_RANK", 0)
+    # test only (tests/test_gpu_multiproc.py): every rank on cuda:0, gloo for
+    # the host-side collectives, the library's collectives through the NCCL
+    # test transport (FMV_NCCL_LIB) -- checks the multi-rank flow of this
+    # script on a one-GPU box; its timings mean nothing
+    shared = os.environ.get("FMV_BENCH_SHARED_GPU") == "1"
+    gpu = 0 if shared else local_rank
     if "WORLD_SIZE" in os.environ and args.impl == "ours" and world != args.gpus and "--gpus" in " ".join(sys.argv):
         raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1 and args.impl == "ours":
         import torch
-
-        if torch.cuda.device_count() < world:
-            raise SystemExit(f"bench: {world} ranks but only {torch.cuda.device_count()} visible GPUs")
-        if local_rank >= torch.cuda.device_count():
-            raise SystemExit(f"bench: LOCAL_RANK {local_rank} has no GPU")
-        import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if shared:
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            if torch.cuda.device_count() < world:
+                raise SystemExit(f"bench: {world} ranks but only {torch.cuda.device_count()} visible GPUs")
+            if local_rank >= torch.cuda.device_count():
+                raise SystemExit(f"bench: LOCAL_RANK {local_rank} has no GPU")
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.impl == "reference":
         line = run_reference_arm(args, rank, world)
     else:
-        line = run_ours(args, rank, world, local_rank)
+        line = run_ours(args, rank, world, gpu)
     if rank == 0 and line is not None:
         print(json.dumps(line), file=json_out, flush=True)
     if world > 1 and args.impl == "ours":
