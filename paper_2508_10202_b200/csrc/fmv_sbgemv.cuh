@@ -567,6 +567,36 @@ __global__ void __launch_bounds__(FMV_SBGEMV_CONS + 32, FMV_SBGEMV_MINB) k_sbgem
       mbar_wait_sleep(&full[s], sg.par);
       const int cnt = (int)sg.cnt;
       auto dot = [&](const E* col, int vi, int vstep, Acc& a0c, Acc& a1c) {
+        if constexpr (std::is_same<E, cf32d>::value) {
+          // 'm': the four real products of each complex MAC go to separate
+          // fp64 accumulators (8 independent DFMA chains per lane instead of
+          // 2 x 2 chains four DFMAs deep per vector), folded at the end
+          double q[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+          auto body4 = [&](double* c, int v0) {
+            const VecT<E, V> a = ldv<E, V>(col + v0 * V);
+            const VecT<E, V> x = ldv<E, V>(Xs + v0 * V);
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              if (V == 1 || !ragged || v0 * V + v < p.m) {
+                const double ax = a.e[v].x, ay = a.e[v].y, xx = x.e[v].x, xy = x.e[v].y;
+                c[0] = fma(ax, xx, c[0]);
+                c[1] = fma(ay, xy, c[1]);
+                c[2] = fma(ax, xy, c[2]);
+                c[3] = fma(ay, xx, c[3]);
+              }
+            }
+          };
+          for (; vi + vstep < MV; vi += 2 * vstep) {
+            body4(q[0], vi);
+            body4(q[1], vi + vstep);
+          }
+          if (vi < MV) body4(q[0], vi);
+          // ConjTrans: conj(a) x = (ax xx + ay xy, ax xy - ay xx); Trans: a x
+          constexpr double sg = MODE == GM_C ? 1.0 : -1.0;
+          a0c = make_double2(q[0][0] + sg * q[0][1], q[0][2] - sg * q[0][3]);
+          a1c = make_double2(q[1][0] + sg * q[1][1], q[1][2] - sg * q[1][3]);
+          return;
+        }
         auto body = [&](Acc& acc, int v0) {
           const VecT<E, V> a = ldv<E, V>(col + v0 * V);
           const VecT<E, V> x = ldv<E, V>(Xs + v0 * V);

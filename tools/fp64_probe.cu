@@ -51,6 +51,28 @@ __global__ void k_reg2(int iters, double* out, long long* clk) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *clk = t1 - t0;
 }
 
+// float -> double conversions (F2F.F64.F32) feeding DFMAs: the 'm' SBGEMV's
+// per-element cost (4 conversions + 4 DFMAs per complex MAC)
+__global__ void k_f2f(int iters, double* out, long long* clk) {
+  float f[8];
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = 1.0f + (threadIdx.x + i) * 1e-7f, a[i] = 0.0;
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma((double)f[i], (double)f[(i + 1) & 7], a[i]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = __int_as_float(__float_as_int(f[i]) ^ 1);  // keep the inputs varying (ALU)
+  }
+  const long long t1 = clock64();
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 1.2345) out[0] = s;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *clk = t1 - t0;
+}
+
 template <int ROWS2>
 __global__ void k_lds(int iters, double* out, long long* clk) {
   __shared__ double2 xs[8 * 64];
@@ -108,20 +130,21 @@ int main() {
   cudaMalloc(&clk, 8);
   const int iters = 20000;
   const int threads[] = {128, 256, 416, 512, 704, 1024};
-  for (int kind = 0; kind < 4; ++kind)
+  for (int kind = 0; kind < 5; ++kind)
     for (int T : threads) {
       for (int w = 0; w < 2; ++w) {
         if (kind == 0) k_reg<<<nsm, T>>>(iters, out, clk);
         else if (kind == 1) k_lds<0><<<nsm, T>>>(iters, out, clk);
         else if (kind == 2) k_lds<1><<<nsm, T>>>(iters, out, clk);
-        else k_reg2<<<nsm, T>>>(iters, out, clk);
+        else if (kind == 3) k_reg2<<<nsm, T>>>(iters, out, clk);
+        else k_f2f<<<nsm, T>>>(iters, out, clk);
       }
       cudaDeviceSynchronize();
       long long c = 0;
       cudaMemcpy(&c, clk, 8, cudaMemcpyDeviceToHost);
-      const double dfma = (double)iters * (kind == 0 ? 16 : kind == 3 ? 20 : 32) * T;  // per CTA (one CTA per SM)
+      const double dfma = (double)iters * (kind == 0 ? 16 : kind == 3 ? 20 : kind == 4 ? 8 : 32) * T;  // per CTA
       printf("%-4s %4d threads/SM: %6.2f DFMA/clk/SM (%s)\n",
-             kind == 0 ? "reg" : kind == 1 ? "lds" : kind == 2 ? "lds2" : "reg2", T,
+             kind == 0 ? "reg" : kind == 1 ? "lds" : kind == 2 ? "lds2" : kind == 3 ? "reg2" : "f2f (DFMA with 2 F2F)", T,
              dfma / (double)c, cudaGetErrorString(cudaGetLastError()));
     }
   return 0;
