@@ -12,8 +12,11 @@ F is N shard-matvecs + an NCCL all-gather of the partial d summed by a fixed tre
 broadcast of d + N shard-matvecs.
 
 value   : shard-matvecs/s of the whole job, device-resident inputs (HBM).
-e2e     : the same through the blocking C-ABI call with pinned HOST buffers
-          (H2D of the input and D2H of the output inside the timed region).
+e2e     : the same through the C ABI with pinned HOST buffers (H2D of every
+          step's inputs and D2H of its outputs inside the timed region):
+          queued calls (fmv_matvec_host_async; each call's copies overlap
+          its neighbours' compute) at N=1, blocking fmv_matvec /
+          fmv_matvec_partitioned otherwise; e2e_blocking: the blocking call.
 roofline: SBGEMV kernels (the dominant phase, ~90% of a matvec) -- reference
           algorithmic bytes nb*(Nd*Nm+Nd+Nm)*16 per launch (gemv.hpp:83-89,
           SURVEY.md §8d) / CUDA-event kernel time, vs MEASURED_PEAKS.json.
@@ -254,7 +257,7 @@ def run_ours(args, rank, world, device):
         if dist is not None:
             dist.barrier()
 
-    def timed(fn, k):
+    def timed(fn, k, join=False):
         barrier()
         ctx.synchronize()
         torch.cuda.synchronize()
@@ -263,6 +266,8 @@ def run_ours(args, rank, world, device):
         e0.record(stream)
         for _ in range(k):
             fn()
+        if join:  # the queued calls' output copies run on a side stream
+            _capi.check(L.fmv_join(ctx.handle))
         e1.record(stream)
         e1.synchronize()
         ctx.synchronize()
@@ -305,9 +310,23 @@ def run_ours(args, rank, world, device):
                 _capi.check(L.fmv_matvec_partitioned(ctx.handle, op.handle, kind, cb, ctypes.c_void_p(x.data_ptr()),
                                                      ctypes.c_void_p(y.data_ptr()), 0, None))
 
+    def step_host_queued():
+        _capi.check(L.fmv_matvec_host_async(ctx.handle, op.handle, 0, cb, ctypes.c_void_p(m_pin.data_ptr()),
+                                            ctypes.c_void_p(do_pin.data_ptr())))
+        _capi.check(L.fmv_matvec_host_async(ctx.handle, op.handle, 1, cb, ctypes.c_void_p(d_pin.data_ptr()),
+                                            ctypes.c_void_p(mo_pin.data_ptr())))
+
     for _ in range(max(3, args.warmup // 2)):
         step_host()
-    ms_e2e = timed(step_host, args.steps)
+    ms_blk = timed(step_host, args.steps)
+    e2e_api = "fmv_matvec (C ABI, blocking), pinned host buffers"
+    ms_e2e = ms_blk
+    if dm is None:
+        for _ in range(max(3, args.warmup // 2)):
+            step_host_queued()
+        ctx.synchronize()
+        ms_e2e = timed(step_host_queued, args.steps, join=True)
+        e2e_api = "fmv_matvec_host_async (C ABI, queued F and F* calls), pinned host buffers"
     clk.__exit__(None, None, None)
     e2e_value = 2 * args.steps * world / (ms_e2e * 1e-3)
     h2d = (NM * NT + ND * NT) * 8 * world
@@ -360,7 +379,10 @@ def run_ours(args, rank, world, device):
         "dtype": "f64" if cfg == "ddddd" else f"mixed:{cfg}", "data": "synthetic (reference uniform_fill, seeded)",
         "config": workload_config(world, cfg),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": ms_e2e / args.steps, "api": "fmv_matvec (C ABI), pinned host buffers"},
+                "ms_per_step": ms_e2e / args.steps, "api": e2e_api},
+        "e2e_blocking": {"value": 2 * args.steps * world / (ms_blk * 1e-3), "unit": UNIT,
+                         "ms_per_step": ms_blk / args.steps,
+                         "api": "fmv_matvec / fmv_matvec_partitioned (C ABI, blocking), pinned host buffers"},
         "gpu_launches": int(launches) * world,
         "roofline": roofline,
         "clocks": clk.summary(),

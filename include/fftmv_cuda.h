@@ -111,6 +111,23 @@ int fmv_matvec_payload(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg
                        double* out, int io_on_device, fmv_phase_times* times);
 /* Non-blocking variant: device pointers only, enqueued on the ctx stream. */
 int fmv_matvec_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* d_in, double* d_out);
+/* Queued host-I/O variant of fmv_matvec (an addition; the reference's
+ * run_pipeline, matvec.hpp:233-289, is blocking): h_in / h_out must be PINNED
+ * host buffers (cudaHostAlloc / cudaHostRegister, else FMV_EINVAL). The call
+ * enqueues the input copy, the pipeline and the output copy and returns
+ * without waiting; results are in h_out after fmv_synchronize(ctx). Two
+ * workspace slots alternate, so consecutive queued calls overlap: call i+1's
+ * input copy (and, for FORWARD, its chunked r2c) runs beside call i's SBGEMV,
+ * and call i's output copy beside call i+1's. Results equal fmv_matvec's
+ * with the same host buffers bit for bit. Do not modify h_in or read h_out
+ * before fmv_synchronize. */
+int fmv_matvec_host_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* h_in,
+                          double* h_out);
+/* Make the ctx stream wait (on the device, no host wait) for the output
+ * copies queued by fmv_matvec_host_async; an event recorded on the ctx stream
+ * afterwards marks the completion of every queued call. fmv_synchronize
+ * includes it. */
+int fmv_join(fmv_ctx* ctx);
 
 /* ---- block (multi-RHS) matvec: SURVEY.md §8 f2 ----
  * nrhs independent inputs back to back (nrhs SOTI vectors of n_in*nt

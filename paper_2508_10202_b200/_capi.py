@@ -59,6 +59,8 @@ def lib() -> ctypes.CDLL:
         "fmv_matvec_payload": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_char, c_void_p, c_void_p, c_int,
                                        POINTER(PhaseTimesC)]),
         "fmv_matvec_async": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_void_p, c_void_p]),
+        "fmv_matvec_host_async": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_void_p, c_void_p]),
+        "fmv_join": (c_int, [c_void_p]),
         "fmv_matvec_block": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_size_t, c_void_p, c_void_p, c_int]),
         "fmv_matvec_block_async": (c_int, [c_void_p, c_void_p, c_int, c_char_p, c_size_t, c_void_p, c_void_p]),
         "fmv_casts_performed": (c_uint64, []),
@@ -103,7 +105,7 @@ def exported_symbols() -> list[str]:
         "fmv_uniform_fill", "fmv_non_representable_fill", "fmv_relative_error", "fmv_fft_r2c", "fmv_fft_c2r",
         "fmv_matvec_block", "fmv_matvec_block_async", "fmv_comm_init_2d", "fmv_matvec_partitioned_2d",
         "fmv_graph_create", "fmv_graph_launch", "fmv_graph_destroy", "fmv_matvec_payload", "fmv_comm_size",
-        "fmv_matvec_partitioned_async", "fmv_host_copy",
+        "fmv_matvec_partitioned_async", "fmv_host_copy", "fmv_matvec_host_async", "fmv_join",
     ]
 
 

@@ -99,12 +99,13 @@ const void* op_bins(fmv_ctx* ctx, fmv_op* op, int prec, long* lda);
 // SBGEMV consumes one, so each chunk's copy hides behind its neighbour's
 // SBGEMV and only the smallest chunk's copy is exposed. Edges on multiples of
 // 4 columns.
-std::vector<long> chunk_edges(const fmv_op* op, int prec2, bool grow) {
+std::vector<long> chunk_edges(const fmv_op* op, int prec2, bool grow, int force = 0) {
   const long nm = (long)op->nm;
   const size_t bytes = op->nb() * op->nm * op->nd * esize(prec2);
   long C = (bytes >= (size_t(1) << 30)) ? 6 : (bytes >= (size_t(1) << 27)) ? 3 : 1;
   const int env = env_int("FMV_CHUNKS", 0);
   if (env > 0) C = env;
+  if (force > 0) C = force;
   C = std::max<long>(1, std::min<long>(C, nm / 4));
   std::vector<double> w(C);
   double tot = 0;
@@ -139,6 +140,12 @@ struct HostIO {
   size_t in_elem = 8;          // bytes per input element (a cfg[0] payload may be float / half)
   unsigned char* pin_in = nullptr;  // staging (set when h_in is pageable)
   double* pin_out = nullptr;        // staging (set when h_out is pageable)
+  // Queued call (fmv_matvec_host_async): pinned buffers only; the copy stream
+  // waits on `guard` (the slot's previous compute) instead of everything
+  // enqueued before, output copies run on the ctx's out_stream and nothing
+  // joins back into the matvec stream.
+  bool queued = false;
+  cudaEvent_t guard = nullptr;
   struct Pending {
     size_t off, count;
     cudaEvent_t ev;
@@ -204,6 +211,10 @@ cudaStream_t copy_stream(fmv_ctx* ctx) {
   if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   return ctx->copy_stream;
 }
+cudaStream_t out_stream(fmv_ctx* ctx) {
+  if (!ctx->out_stream) CK(cudaStreamCreateWithFlags(&ctx->out_stream, cudaStreamNonBlocking));
+  return ctx->out_stream;
+}
 cudaEvent_t chunk_event(fmv_ctx* ctx, int i) {
   if (!ctx->cev[i]) CK(cudaEventCreateWithFlags(&ctx->cev[i], cudaEventDisableTiming));
   return ctx->cev[i];
@@ -238,12 +249,20 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const Cfg& p, const voi
   // (Device-resident F split the same way -- each chunk's r2c on the copy
   // stream beside the previous chunk's SBGEMV -- was measured slower: 1.206 ms
   // per F unchunked, 1.22 / 1.23 / 1.24 / 1.26 ms with 2 / 3 / 4 / 6 chunks.)
-  const std::vector<long> edges = (h_in || h_out) ? chunk_edges(op, p[2], fwd) : std::vector<long>{0, (long)op->nm};
+  // Queued calls overlap their copies with the neighbouring calls instead, so
+  // they run unchunked by default (FMV_QCHUNKS: 1 -> 820, 2 -> 816, 3 -> 807,
+  // 6 -> 784 e2e matvecs/s at C2; device-resident 817).
+  const int qchunks = hio && hio->queued ? env_int("FMV_QCHUNKS", 1) : 0;
+  const std::vector<long> edges =
+      (h_in || h_out) ? chunk_edges(op, p[2], fwd, qchunks) : std::vector<long>{0, (long)op->nm};
   const int C = (int)edges.size() - 1;
   auto chunk_edge = [&](long, int c, int) { return edges[c]; };
   cudaStream_t cs = ctx->stream;
   if (C > 16) fail(FMV_EINVAL, "too many chunks");
-  if (h_in || h_out) {  // the copy stream must not run ahead into a buffer still in use
+  const bool queued = hio && hio->queued;
+  if (queued) {  // only this slot's previous compute may still read its buffers
+    CK(cudaStreamWaitEvent(copy_stream(ctx), hio->guard, 0));
+  } else if (h_in || h_out) {  // the copy stream must not run ahead into a buffer still in use
     CK(cudaEventRecord(chunk_event(ctx, 32), cs));
     CK(cudaStreamWaitEvent(copy_stream(ctx), chunk_event(ctx, 32), 0));
   }
@@ -335,13 +354,24 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const Cfg& p, const voi
       for (int c = 0; c < C; ++c) gemv_chunk(c);
     }
     c2r_series(0, n_out);
-    if (h_out) hio->d2h(ctx, 0, out, (size_t)n_out * nt, cs, chunk_event(ctx, 16));
+    if (h_out && queued) {  // the next call's compute does not wait for this copy
+      CK(cudaEventRecord(chunk_event(ctx, 30), cs));
+      CK(cudaStreamWaitEvent(out_stream(ctx), chunk_event(ctx, 30), 0));
+      hio->d2h(ctx, 0, out, (size_t)n_out * nt, out_stream(ctx), nullptr);
+    } else if (h_out) {
+      hio->d2h(ctx, 0, out, (size_t)n_out * nt, cs, chunk_event(ctx, 16));
+    }
   } else {
-    if (h_in)
+    if (h_in && queued) {  // copied beside the previous call's compute
+      hio->h2d(ctx, const_cast<void*>(in), 0, (size_t)n_in * nt * hio->in_elem, copy_stream(ctx));
+      CK(cudaEventRecord(chunk_event(ctx, 31), copy_stream(ctx)));
+      CK(cudaStreamWaitEvent(cs, chunk_event(ctx, 31), 0));
+    } else if (h_in) {
       hio->h2d(ctx, const_cast<void*>(in), 0, (size_t)n_in * nt * hio->in_elem, cs);
+    }
     r2c_series(0, n_in);
     if (h_out) {
-      cudaStream_t ks = copy_stream(ctx);
+      cudaStream_t ks = queued ? out_stream(ctx) : copy_stream(ctx);
       // (chunk c's c2r stays on the matvec stream: on the copy stream, running
       // alongside the SBGEMV of chunk c+1, it slowed F* from 1.37 to 1.62 ms
       // with a full grid and to 2.13 ms with one-CTA-per-SM sub-launches --
@@ -363,8 +393,10 @@ void pipeline(fmv_ctx* ctx, const fmv_op* cop, int kind, const Cfg& p, const voi
         if (c > 0) issue_out(c - 1);
       }
       issue_out(C - 1);
-      CK(cudaEventRecord(chunk_event(ctx, 33), ks));
-      CK(cudaStreamWaitEvent(cs, chunk_event(ctx, 33), 0));
+      if (!queued) {
+        CK(cudaEventRecord(chunk_event(ctx, 33), ks));
+        CK(cudaStreamWaitEvent(cs, chunk_event(ctx, 33), 0));
+      }
     } else {
       for (int c = 0; c < C; ++c) gemv_chunk(c);
       c2r_series(0, n_out);
@@ -621,6 +653,19 @@ double env_seconds(const char* name, double dflt) {
 // -- which also unblocks kernels stuck waiting for a dead peer -- and fails
 // the call with FMV_ENCCL instead of hanging forever. The context then has
 // no communicator; fmv_comm_init must be called again.
+// Make the matvec stream wait for everything enqueued on the side streams
+// (queued host-I/O output copies), without a host wait.
+void join_side_streams(fmv_ctx* ctx) {
+  int i = 28;
+  for (cudaStream_t side : {ctx->copy_stream, ctx->out_stream}) {
+    if (side) {
+      CK(cudaEventRecord(chunk_event(ctx, i), side));
+      CK(cudaStreamWaitEvent(ctx->stream, chunk_event(ctx, i), 0));
+    }
+    ++i;
+  }
+}
+
 void comm_sync(fmv_ctx* ctx) {
   void* comms[3] = {ctx->comm, ctx->row_comm, ctx->col_comm};
   const bool any = comms[0] || comms[1] || comms[2];
@@ -761,12 +806,18 @@ int fmv_ctx_destroy(fmv_ctx* ctx) {
     if (!ctx) return;
     DeviceGuard dg(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+    if (ctx->out_stream) cudaStreamSynchronize(ctx->out_stream);
     for (auto* b : {&ctx->x, &ctx->y, &ctx->yacc, &ctx->io_in, &ctx->io_out, &ctx->partials, &ctx->counters,
-                    &ctx->payload, &ctx->red, &ctx->fft_scratch})
+                    &ctx->payload, &ctx->red, &ctx->fft_scratch, &ctx->q_x[0], &ctx->q_x[1], &ctx->q_in[0],
+                    &ctx->q_in[1], &ctx->q_out_buf[0], &ctx->q_out_buf[1], &ctx->q_scr[0], &ctx->q_scr[1]})
       b->release();
     ctx->pin_in.release();
     ctx->pin_out.release();
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->out_stream) cudaStreamDestroy(ctx->out_stream);
+    for (auto e : {ctx->q_done[0], ctx->q_done[1], ctx->q_out[0], ctx->q_out[1]})
+      if (e) cudaEventDestroy(e);
     for (auto e : ctx->cev)
       if (e) cudaEventDestroy(e);
     for (auto& r : ctx->prof) {
@@ -821,7 +872,16 @@ int fmv_synchronize(fmv_ctx* ctx) {
   return guarded([&] {
     if (!ctx) fail(FMV_EINVAL, "null ctx");
     DeviceGuard dg(ctx->device);
+    join_side_streams(ctx);
     comm_sync(ctx);  // a plain stream sync without communicators
+  });
+}
+
+int fmv_join(fmv_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) fail(FMV_EINVAL, "null ctx");
+    DeviceGuard dg(ctx->device);
+    join_side_streams(ctx);
   });
 }
 
@@ -994,6 +1054,51 @@ int fmv_matvec(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const 
     const auto p = parse_cfg(cfg);
     DeviceGuard dg(ctx->device);
     matvec_blocking(ctx, op, kind, p, -1, in, out, io_on_device != 0, times);
+  });
+}
+
+int fmv_matvec_host_async(fmv_ctx* ctx, const fmv_op* op, int kind, const char* cfg, const double* h_in,
+                          double* h_out) {
+  return guarded([&] {
+    NvtxRange nr(nvtx_matvec_name("matvec_host_async", kind, cfg));
+    if (!ctx || !op || !h_in || !h_out) fail(FMV_EINVAL, "fmv_matvec_host_async: null argument");
+    if (kind != FMV_FORWARD && kind != FMV_ADJOINT) fail(FMV_EINVAL, "matvec: bad kind");
+    check_same_device(ctx, op);
+    const auto p = parse_cfg(cfg);
+    DeviceGuard dg(ctx->device);
+    if (is_pageable(h_in) || is_pageable(h_out))
+      fail(FMV_EINVAL, "fmv_matvec_host_async: host buffers must be pinned (cudaHostAlloc / cudaHostRegister)");
+    const bool fwd = kind == FMV_FORWARD;
+    const size_t n_in = (fwd ? op->nm : op->nd) * op->nt, n_out = (fwd ? op->nd : op->nm) * op->nt;
+    const int s = ctx->q_slot;
+    for (cudaEvent_t* e : {&ctx->q_done[s], &ctx->q_out[s]})
+      if (!*e) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    // slot s's output buffer was last read by the copy-out of the call two back
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->q_out[s], 0));
+    // the pipeline works on ctx->x / io_in / io_out: lend it this slot's buffers
+    struct Lend {
+      fmv_ctx* c;
+      int s;
+      Lend(fmv_ctx* c_, int s_) : c(c_), s(s_) { swap(); }
+      ~Lend() { swap(); }
+      void swap() {
+        std::swap(c->x, c->q_x[s]);
+        std::swap(c->io_in, c->q_in[s]);
+        std::swap(c->io_out, c->q_out_buf[s]);
+        std::swap(c->fft_scratch, c->q_scr[s]);  // runtime-plan FFTs of the two slots may overlap
+      }
+    } lend(ctx, s);
+    ctx->io_in.ensure(n_in * sizeof(double));
+    ctx->io_out.ensure(n_out * sizeof(double));
+    HostIO hio;
+    hio.h_in = h_in;
+    hio.h_out = h_out;
+    hio.queued = true;
+    hio.guard = ctx->q_done[s];
+    pipeline(ctx, op, kind, p, ctx->io_in.p, -1, static_cast<double*>(ctx->io_out.p), &hio);
+    CK(cudaEventRecord(ctx->q_done[s], ctx->stream));
+    CK(cudaEventRecord(ctx->q_out[s], out_stream(ctx)));
+    ctx->q_slot = s ^ 1;
   });
 }
 

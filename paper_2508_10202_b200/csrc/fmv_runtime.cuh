@@ -339,6 +339,15 @@ struct fmv_ctx {
   PinBuf pin_in, pin_out;  // staging for pageable host I/O (HostIO)
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t cev[34] = {};
+  // Queued host-I/O matvecs (fmv_matvec_host_async): two buffer slots used
+  // alternately, so call i+1's input copy and r2c (copy_stream) run while
+  // call i computes, and call i's output copy (out_stream) while call i+1
+  // computes. q_done[s]: slot s's last compute finished (recorded on
+  // `stream`); q_out[s]: its output copy finished (on out_stream).
+  cudaStream_t out_stream = nullptr;
+  DevBuf q_x[2], q_in[2], q_out_buf[2], q_scr[2];
+  cudaEvent_t q_done[2] = {}, q_out[2] = {};
+  int q_slot = 0;
   size_t counters_len = 0;
   uint64_t launches = 0;
   bool profiling = false;

@@ -33,7 +33,7 @@ __all__ = [
     "setup_operator", "materialize_single", "MatvecKind", "PhaseTimings", "MatvecResult", "phase_name",
     "forward_matvec", "adjoint_matvec", "run_pipeline", "Context", "default_context", "casts_performed",
     "reset_cast_counter", "uniform_fill", "seed_stream", "non_representable_fill", "relative_error", "FmvError",
-    "matvec_block", "forward_matvec_block", "adjoint_matvec_block", "MatvecGraph",
+    "matvec_block", "forward_matvec_block", "adjoint_matvec_block", "MatvecGraph", "matvec_host_async",
 ]
 
 
@@ -482,6 +482,22 @@ def adjoint_matvec(op: SpectralOperator, d: BlockVector, cfg="ddddd", tiling=Non
     _check_input(op, d, False)
     out, t = run_pipeline(op, MatvecKind.Adjoint, d.data, cfg, timings=timings)
     return MatvecResult(BlockVector.time_double(op.dims.n_m, op.dims.n_t, out), t)
+
+
+def matvec_host_async(op: SpectralOperator, kind: MatvecKind, x, y, cfg="ddddd", ctx: Optional[Context] = None):
+    """Queued host-I/O matvec (fmv_matvec_host_async): ``x``
+    and ``y`` are PINNED host torch float64 tensors (n_in*nt / n_out*nt);
+    the call enqueues the copies and the pipeline and returns at once.
+    ``y`` holds the result after ``ctx.synchronize()``; consecutive calls
+    overlap each other's copies with their SBGEMVs."""
+    ctx = ctx or op.ctx
+    fwd = kind == MatvecKind.Forward
+    n_in = (op.dims.n_m if fwd else op.dims.n_d) * op.dims.n_t
+    n_out = (op.dims.n_d if fwd else op.dims.n_m) * op.dims.n_t
+    if x.numel() != n_in or y.numel() != n_out:
+        raise ValueError("matvec: input length does not match operator dims")
+    check(lib().fmv_matvec_host_async(ctx.handle, op.handle, 0 if fwd else 1, _cfg_str(cfg).encode(),
+                                      ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr())))
 
 
 def matvec_block(op: SpectralOperator, kind: MatvecKind, inp, cfg="ddddd", ctx: Optional[Context] = None):
