@@ -293,9 +293,9 @@ bool plan_block(GemvPlan& gp, int mode, size_t es, size_t accsz, int KR) {
   return gp.smem <= 227 * 1024 && (long)(p.Jc - 1) * p.lda * (long)es + p.m * (long)es <= 96 * 1024;
 }
 
-template <int MODE, class E, class O, int KR, int LPC, int KX = 0, int XR = 0>
+template <int MODE, class E, class O, int KR, int LPC, int KX = 0, int XR = 0, int TC = 0>
 void sbgemm_block_launch_t(fmv_ctx* ctx, GemvPlan& gp) {
-  auto kern = k_sbgemm_block<MODE, E, O, KR, LPC, KX, XR>;
+  auto kern = k_sbgemm_block<MODE, E, O, KR, LPC, KX, XR, TC>;
   prep_smem((const void*)kern, gp.smem);
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, gp.block, gp.smem));
@@ -319,6 +319,38 @@ bool sbgemm_block_t(fmv_ctx* ctx, GemvPlan& gp) {
   // ConjTrans lanes per column: 8 for columns up to 128 elements, else a warp
   constexpr int L1 = MODE == GM_N ? 0 : 8, L2 = MODE == GM_N ? 0 : 32;
   const bool wide = MODE != GM_N && gp.p.m > 128;
+  if constexpr (MODE == GM_N && std::is_same<E, double2>::value) {
+    // DMMA variant (K = 8, 88 < m <= 104: all 13 row tiles live): nw consumer warps, stages of exactly
+    // one column pair per warp, x slices 544 B apart (off the 128-byte bank
+    // period), one K*m reduction buffer
+    constexpr int kTC = 13, XRT = 544;
+    const int nw = env_int("FMV_BLOCK_TC_WARPS", 8);
+    GemvParams& q = gp.p;
+    if (K == 8 && q.m <= 8 * kTC && q.m > 8 * (kTC - 2) && env_int("FMV_BLOCK_TC", 1) && nw >= 1 && nw <= 8) {
+      auto up128 = [](long v) { return (int)((v + 127) / 128 * 128); };
+      // two column pairs per warp per stage (tools/bench_block.py, C2 K = 8 SBGEMV:
+      // 1 pair 2.02 ms, 2 pairs 1.575 ms; CUDA-core exact-K kernel 1.754 ms)
+      const int Jc = 2 * nw * std::max(1, env_int("FMV_BLOCK_TC_PAIRS", 2));
+      const long a_bytes = ((long)(Jc - 1) * q.lda + q.m) * 16;
+      const int a_slot = up128(a_bytes + 32);
+      const size_t red = (size_t)(8 * q.m * 16 + 127) / 128 * 128;
+      int ns = std::min(8, std::max(2, env_int("FMV_BLOCK_TC_STAGES", 8)));
+      auto smem_of = [&](int n) { return (size_t)512 + (size_t)n * (a_slot + 8 * XRT) + red; };
+      while (ns > 2 && smem_of(ns) > 227 * 1024) --ns;
+      if (Jc * 16 + 32 <= XRT && smem_of(ns) <= 227 * 1024 && a_bytes <= 120 * 1024) {
+        q.Jc = Jc;
+        q.a_slot = a_slot;
+        q.xr_slot = XRT;
+        q.nstage = ns;
+        q.G = 1;
+        q.RT = q.m;
+        gp.smem = smem_of(ns);
+        gp.block = nw * 32 + 32;
+        sbgemm_block_launch_t<MODE, E, O, 8, L1, 8, XRT, kTC>(ctx, gp);
+        return true;
+      }
+    }
+  }
   if constexpr (MODE == GM_N && std::is_same<E, double2>::value) {
     // exact-K variant with a fixed 1 KB x-slice stride (stages of <= 62 columns)
     constexpr int XR = 1024;

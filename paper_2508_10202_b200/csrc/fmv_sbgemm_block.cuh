@@ -36,14 +36,28 @@ namespace fmv {
 #ifndef FMV_BLOCK_MINB
 #define FMV_BLOCK_MINB 1  // resident CTAs per SM
 #endif
+// D += A B for one 8x8x4 fp64 tile held in PTX m8n8k4 fragments (DMMA).
+__device__ __forceinline__ void dmma_884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
 // KX > 0, NoTrans fp64: exactly KX = KR right-hand sides and x slices XR
 // bytes apart in shared memory, both compile-time -- the column loop then has
 // no per-RHS predicates and every x read is one LDS.128 at an immediate offset
 // from a single per-column base (the runtime-K loop spent ~30 integer /
 // predicate instructions per 32 DFMAs on this).
 // KX > 0, ConjTrans: exactly KX right-hand sides, two columns per lane.
-template <int MODE, class E, class O, int KR, int LPC, int KX = 0, int XR = 0>
-__global__ void __launch_bounds__(FMV_BLOCK_CONS + 32, FMV_BLOCK_MINB) k_sbgemm_block(const GemvParams p) {
+// TC > 0, NoTrans fp64 with KX = 8: the complex MACs run on the FP64 tensor
+// path (DMMA, mma.sync m8n8k4 f64) for up to TC row tiles of 8 (m <= 8 TC):
+// see the TC branch below.
+// (TC: at most 8 consumer warps + the producer, <= 3 warps per SM
+// sub-partition, so ptxas may give each thread 168 registers: the 13 tiles'
+// 104 accumulator registers plus 26 for the A fragments without spills.)
+template <int MODE, class E, class O, int KR, int LPC, int KX = 0, int XR = 0, int TC = 0>
+__global__ void __launch_bounds__(TC > 0 ? 8 * 32 + 32 : FMV_BLOCK_CONS + 32, FMV_BLOCK_MINB)
+    k_sbgemm_block(const GemvParams p) {
   using Tr = ET<E>;
   using Acc = typename Tr::A;
   extern __shared__ __align__(128) unsigned char sm[];
@@ -131,6 +145,18 @@ __global__ void __launch_bounds__(FMV_BLOCK_CONS + 32, FMV_BLOCK_MINB) k_sbgemm_
     for (int k = 0; k < KR; ++k) acc[k] = cmp[k] = Tr::zero();
 #pragma unroll
     for (int k = 0; k < (kSplit ? KR : 1); ++k) rr[k] = ii[k] = ri[k] = ir[k] = 0.0;
+    // TC: warp w takes column pairs w, w + nw, ... of each stage; per pair and
+    // row tile one 8-byte A load per lane feeds two DMMAs (real and imaginary
+    // part of Y for all 8 right-hand sides). The real-ified product is
+    //   Yr = [Ar Ai] [Xr; -Xi],  Yi = [Ar Ai] [Xi; Xr]
+    // with the k index (column j, component c) matching the interleaved
+    // complex layout of A, so A needs no reshuffle. Lane (g = lane/4, q =
+    // lane%4) holds A[row 8T+g][k = q] = component q&1 of column 2jp + q/2,
+    // B[k = q][rhs g], and D[row 8T+g][rhs 2q, 2q+1] (PTX m8n8k4 fragments).
+    constexpr int TCT = TC > 0 ? TC : 1;
+    double tR[TCT][2], tI[TCT][2];
+#pragma unroll
+    for (int T = 0; T < TCT; ++T) tR[T][0] = tR[T][1] = tI[T][0] = tI[T][1] = 0.0;
     for (SegIter sg(c0, c1, p); sg.more(); sg.advance(p)) {
       sg.load(p);
       const int s = sg.s;
@@ -140,7 +166,37 @@ __global__ void __launch_bounds__(FMV_BLOCK_CONS + 32, FMV_BLOCK_MINB) k_sbgemm_
       // x slice r starts at its slot + the source's offset within 16 bytes
       const unsigned char* xbase = base + p.a_slot;
       mbar_wait_sleep(&full[s], sg.par);
-      if (active && kSplit) {
+      if constexpr (TC > 0) {
+        static_assert(KX == 8 && KR == 8 && kSplit, "DMMA variant: fp64, exactly 8 right-hand sides");
+        const int w = t >> 5, nw = ncons >> 5;
+        const int q = lane & 3, g8 = lane >> 2;
+        const int cnt = (int)sg.cnt;
+        const int npair = (cnt + 1) >> 1;
+        const unsigned char* x0 = p.x + (sg.b * p.sx + sg.j) * es;
+        const unsigned char* xs = xbase + (reinterpret_cast<uintptr_t>(x0) & 15) + (long)g8 * XR;
+        for (int jp = w; jp < npair; jp += nw) {
+          const int jj = 2 * jp + (q >> 1);
+          const bool vc = jj < cnt;
+          const double2 xv = vc ? *reinterpret_cast<const double2*>(xs + jj * 16) : make_double2(0.0, 0.0);
+          const double bR = (q & 1) ? -xv.y : xv.x;
+          const double bI = (q & 1) ? xv.x : xv.y;
+          const double* ac = reinterpret_cast<const double*>(As + (long)jj * p.lda) + (q & 1);
+          // all tiles' A fragments first (no per-tile branch: the host only
+          // picks this variant for m > 8 (TC - 1) - 8, so every tile is live),
+          // so the shared-load latency is paid once per column pair
+          double a[TCT];
+#pragma unroll
+          for (int T = 0; T < TCT; ++T) {
+            const int row = T * 8 + g8;
+            a[T] = (vc && row < p.m) ? ac[2 * row] : 0.0;
+          }
+#pragma unroll
+          for (int T = 0; T < TCT; ++T) {
+            dmma_884(tR[T], a[T], bR);
+            dmma_884(tI[T], a[T], bI);
+          }
+        }
+      } else if (active && kSplit) {
         if constexpr (kSplit) {
           const int cnt = (int)sg.cnt;
           const E* Xs[KR];
@@ -212,7 +268,32 @@ __global__ void __launch_bounds__(FMV_BLOCK_CONS + 32, FMV_BLOCK_MINB) k_sbgemm_
       if (p.arrive_all || lane == 0) mbar_arrive(&empty[s]);
       if (sg.ends_bin(p)) {
         const int KM = K * p.m;
-        if (active) {
+        if constexpr (TC > 0) {
+          // the warps' partial sums are added into red in warp order (fixed,
+          // so the result is deterministic); p.G == 1 below
+          const int w = t >> 5, nw = ncons >> 5;
+          const int q = lane & 3, g8 = lane >> 2;
+          const int mt = (p.m + 7) >> 3;
+          for (int ww = 0; ww < nw; ++ww) {
+            if (w == ww) {
+#pragma unroll
+              for (int T = 0; T < TCT; ++T) {
+                const int row = T * 8 + g8;
+                if (T < mt && row < p.m) {
+#pragma unroll
+                  for (int e = 0; e < 2; ++e) {
+                    const int i = (2 * q + e) * p.m + row;
+                    const double2 v = make_double2(tR[T][e], tI[T][e]);
+                    red[i] = ww == 0 ? v : Tr::add(red[i], v);
+                  }
+                }
+              }
+            }
+            bar_consumers(ncons);
+          }
+#pragma unroll
+          for (int T = 0; T < TCT; ++T) tR[T][0] = tR[T][1] = tI[T][0] = tI[T][1] = 0.0;
+        } else if (active) {
 #pragma unroll
           for (int k = 0; k < KR; ++k) {
             if constexpr (kSplit) {
