@@ -320,17 +320,20 @@ bool sbgemm_block_t(fmv_ctx* ctx, GemvPlan& gp) {
   constexpr int L1 = MODE == GM_N ? 0 : 8, L2 = MODE == GM_N ? 0 : 32;
   const bool wide = MODE != GM_N && gp.p.m > 128;
   if constexpr (MODE == GM_N && std::is_same<E, double2>::value) {
-    // DMMA variant (K = 8, 88 < m <= 104: all 13 row tiles live): nw consumer warps, stages of exactly
-    // one column pair per warp, x slices 544 B apart (off the 128-byte bank
-    // period), one K*m reduction buffer
-    constexpr int kTC = 13, XRT = 544;
-    const int nw = env_int("FMV_BLOCK_TC_WARPS", 8);
+    // DMMA variant (K = 8, 88 < m <= 104: 13 row tiles of 8, 7 + 6 per warp
+    // pair): nw consumer warps in nw/2 pairs, stages of exactly P column pairs
+    // per warp pair, x slices 544 B apart (off the 128-byte bank period), one
+    // K*m reduction buffer
+    constexpr int kTC = 7, XRT = 544;  // tiles per warp: a warp pair covers 13 row tiles
+    const int nw = env_int("FMV_BLOCK_TC_WARPS", 16);
     GemvParams& q = gp.p;
-    if (K == 8 && q.m <= 8 * kTC && q.m > 8 * (kTC - 2) && env_int("FMV_BLOCK_TC", 1) && nw >= 1 && nw <= 8) {
+    if (K == 8 && q.m <= 8 * (2 * kTC - 1) && q.m > 8 * (2 * kTC - 3) && env_int("FMV_BLOCK_TC", 1) &&
+        (nw == 8 || nw == 16)) {
       auto up128 = [](long v) { return (int)((v + 127) / 128 * 128); };
-      // two column pairs per warp per stage (tools/bench_block.py, C2 K = 8 SBGEMV:
-      // 1 pair 2.02 ms, 2 pairs 1.575 ms; CUDA-core exact-K kernel 1.754 ms)
-      const int Jc = 2 * nw * std::max(1, env_int("FMV_BLOCK_TC_PAIRS", 2));
+      // P = 2 column pairs per warp pair and stage (tools/bench_block.py, C2 K = 8
+      // SBGEMV; the first design, one warp per column pair with all 13 tiles and
+      // 8 warps: 1 pair 2.02 ms, 2 pairs 1.575 ms; CUDA-core kernel 1.754 ms)
+      const int Jc = nw * std::max(1, env_int("FMV_BLOCK_TC_PAIRS", 2));
       const long a_bytes = ((long)(Jc - 1) * q.lda + q.m) * 16;
       const int a_slot = up128(a_bytes + 32);
       const size_t red = (size_t)(8 * q.m * 16 + 127) / 128 * 128;

@@ -52,11 +52,11 @@ __device__ __forceinline__ void dmma_884(double (&d)[2], double a, double b) {
 // TC > 0, NoTrans fp64 with KX = 8: the complex MACs run on the FP64 tensor
 // path (DMMA, mma.sync m8n8k4 f64) for up to TC row tiles of 8 (m <= 8 TC):
 // see the TC branch below.
-// (TC: at most 8 consumer warps + the producer, <= 3 warps per SM
-// sub-partition, so ptxas may give each thread 168 registers: the 13 tiles'
-// 104 accumulator registers plus 26 for the A fragments without spills.)
+// (TC: up to 16 consumer warps + the producer; a warp holds TC tiles' 8 TC
+// accumulator registers, so the 96 registers of 5 warps per SM sub-partition
+// suffice.)
 template <int MODE, class E, class O, int KR, int LPC, int KX = 0, int XR = 0, int TC = 0>
-__global__ void __launch_bounds__(TC > 0 ? 8 * 32 + 32 : FMV_BLOCK_CONS + 32, FMV_BLOCK_MINB)
+__global__ void __launch_bounds__(TC > 0 ? 16 * 32 + 32 : FMV_BLOCK_CONS + 32, FMV_BLOCK_MINB)
     k_sbgemm_block(const GemvParams p) {
   using Tr = ET<E>;
   using Acc = typename Tr::A;
@@ -145,7 +145,9 @@ __global__ void __launch_bounds__(TC > 0 ? 8 * 32 + 32 : FMV_BLOCK_CONS + 32, FM
     for (int k = 0; k < KR; ++k) acc[k] = cmp[k] = Tr::zero();
 #pragma unroll
     for (int k = 0; k < (kSplit ? KR : 1); ++k) rr[k] = ii[k] = ri[k] = ir[k] = 0.0;
-    // TC: warp w takes column pairs w, w + nw, ... of each stage; per pair and
+    // TC: the consumer warps form nw/2 warp pairs; pair wp takes column pairs
+    // wp, wp + nw/2, ... of each stage, its first warp row tiles 0..TC-1, its
+    // second TC..2TC-2 (13 tiles of 8 rows for m <= 104). Per column pair and
     // row tile one 8-byte A load per lane feeds two DMMAs (real and imaginary
     // part of Y for all 8 right-hand sides). The real-ified product is
     //   Yr = [Ar Ai] [Xr; -Xi],  Yi = [Ar Ai] [Xi; Xr]
@@ -168,32 +170,37 @@ __global__ void __launch_bounds__(TC > 0 ? 8 * 32 + 32 : FMV_BLOCK_CONS + 32, FM
       mbar_wait_sleep(&full[s], sg.par);
       if constexpr (TC > 0) {
         static_assert(KX == 8 && KR == 8 && kSplit, "DMMA variant: fp64, exactly 8 right-hand sides");
-        const int w = t >> 5, nw = ncons >> 5;
+        const int w = t >> 5, nwp = ncons >> 6;
+        const int half = (w >> 2) & 1, wp = (w & 3) + 4 * (w >> 3);
         const int q = lane & 3, g8 = lane >> 2;
         const int cnt = (int)sg.cnt;
         const int npair = (cnt + 1) >> 1;
         const unsigned char* x0 = p.x + (sg.b * p.sx + sg.j) * es;
         const unsigned char* xs = xbase + (reinterpret_cast<uintptr_t>(x0) & 15) + (long)g8 * XR;
-        for (int jp = w; jp < npair; jp += nw) {
+#pragma unroll 2
+        for (int jp = wp; jp < npair; jp += nwp) {
           const int jj = 2 * jp + (q >> 1);
           const bool vc = jj < cnt;
           const double2 xv = vc ? *reinterpret_cast<const double2*>(xs + jj * 16) : make_double2(0.0, 0.0);
           const double bR = (q & 1) ? -xv.y : xv.x;
           const double bI = (q & 1) ? xv.x : xv.y;
-          const double* ac = reinterpret_cast<const double*>(As + (long)jj * p.lda) + (q & 1);
-          // all tiles' A fragments first (no per-tile branch: the host only
-          // picks this variant for m > 8 (TC - 1) - 8, so every tile is live),
-          // so the shared-load latency is paid once per column pair
+          const double* ac =
+              reinterpret_cast<const double*>(As + (long)jj * p.lda + half * TCT * 8) + (q & 1);
+          // all tiles' A fragments first, so the shared-load latency is paid
+          // once per column pair; the second warp's last tile (rows 8(2TC-1)..)
+          // is not live (warp-uniform skip)
           double a[TCT];
 #pragma unroll
           for (int T = 0; T < TCT; ++T) {
-            const int row = T * 8 + g8;
-            a[T] = (vc && row < p.m) ? ac[2 * row] : 0.0;
+            const int row = (half * TCT + T) * 8 + g8;
+            a[T] = (vc && row < p.m) ? ac[2 * (T * 8 + g8)] : 0.0;
           }
 #pragma unroll
           for (int T = 0; T < TCT; ++T) {
-            dmma_884(tR[T], a[T], bR);
-            dmma_884(tI[T], a[T], bI);
+            if (T < TCT - 1 || half == 0) {
+              dmma_884(tR[T], a[T], bR);
+              dmma_884(tI[T], a[T], bI);
+            }
           }
         }
       } else if (active && kSplit) {
@@ -271,20 +278,21 @@ __global__ void __launch_bounds__(TC > 0 ? 8 * 32 + 32 : FMV_BLOCK_CONS + 32, FM
         if constexpr (TC > 0) {
           // the warps' partial sums are added into red in warp order (fixed,
           // so the result is deterministic); p.G == 1 below
+          // (warp pair 0 -- warps 0 and 4 -- stores its rows first)
           const int w = t >> 5, nw = ncons >> 5;
+          const int half = (w >> 2) & 1, wp = (w & 3) + 4 * (w >> 3);
           const int q = lane & 3, g8 = lane >> 2;
-          const int mt = (p.m + 7) >> 3;
           for (int ww = 0; ww < nw; ++ww) {
             if (w == ww) {
 #pragma unroll
               for (int T = 0; T < TCT; ++T) {
-                const int row = T * 8 + g8;
-                if (T < mt && row < p.m) {
+                const int row = (half * TCT + T) * 8 + g8;
+                if (row < p.m) {
 #pragma unroll
                   for (int e = 0; e < 2; ++e) {
                     const int i = (2 * q + e) * p.m + row;
                     const double2 v = make_double2(tR[T][e], tI[T][e]);
-                    red[i] = ww == 0 ? v : Tr::add(red[i], v);
+                    red[i] = wp == 0 ? v : Tr::add(red[i], v);
                   }
                 }
               }
