@@ -322,9 +322,9 @@ bool sbgemm_block_t(fmv_ctx* ctx, GemvPlan& gp) {
   if constexpr (MODE == GM_N && std::is_same<E, double2>::value) {
     // DMMA variant (K = 8, 88 < m <= 104: 13 row tiles of 8, 7 + 6 per warp
     // pair): nw consumer warps in nw/2 pairs, stages of exactly P column pairs
-    // per warp pair, x slices 544 B apart (off the 128-byte bank period), one
+    // per warp pair, x slices 800 B apart (off the 128-byte bank period), one
     // K*m reduction buffer
-    constexpr int kTC = 7, XRT = 544;  // tiles per warp: a warp pair covers 13 row tiles
+    constexpr int kTC = 7, XRT = 800;  // tiles per warp: a warp pair covers 13 row tiles; x slot for <= 48 columns
     const int nw = env_int("FMV_BLOCK_TC_WARPS", 16);
     GemvParams& q = gp.p;
     if (K == 8 && q.m <= 8 * (2 * kTC - 1) && q.m > 8 * (2 * kTC - 3) && env_int("FMV_BLOCK_TC", 1) &&
